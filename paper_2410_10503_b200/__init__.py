@@ -1,0 +1,21 @@
+"""B200-native motion-compensated PDHG / SPDHG reconstruction (arXiv 2410.10503).
+
+Drop-in for the hot path of the reference package ``mctomo``: the gated
+operators A_i = A o D_i (Joseph ray transform after a rigid / dilatation /
+dense warp), step-size selection, and the PDHG / SPDHG solver entry points,
+computed by hand-written sm_100a kernels behind a C-ABI
+(include/mctomo_b200.h).  There is no CPU fallback.
+"""
+
+from .build import build_native
+from .experiment_io import ConvergenceRecord, rmse
+from .functionals import fit_value, g_value, moduli, prox_fstar, prox_g
+from .linops import (ComposedMap, GramSumMap, LinearMap, adjoint_mismatch, compose,
+                     power_method, stacked_norm_sq)
+from .motion import DenseWarpOperator, MotionParams, WarpOperator, motion_sequence
+from .projector import Geometry, GatedOperator, RayTransform, adjoint, forward, ray_transform
+from .simulate import estimate_norms, gate_operators, gaussian_field, simulate_data
+from .solvers import (RHO, DivergenceError, Problem, SaddlePoint, SolverConfig, SolverState,
+                      default_config, draw_sequence, run, run_batch, sample_gates, step)
+
+__version__ = "0.1.0"

@@ -1,0 +1,671 @@
+// C-ABI layer (include/mctomo_b200.h): argument validation, plan construction,
+// workspace layout and kernel launches.  No torch types cross this boundary.
+#include "mct_internal.cuh"
+
+#include <math.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+namespace {
+thread_local std::string g_err;
+
+inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+inline int cuda_fail(cudaError_t e, const char* where) {
+    return mct_set_error(MCT_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define MCT_CUDA(call, where)                         \
+    do {                                              \
+        cudaError_t _e = (call);                      \
+        if (_e != cudaSuccess) return cuda_fail(_e, where); \
+    } while (0)
+
+#define MCT_REQUIRE(cond, msg)                                       \
+    do {                                                             \
+        if (!(cond)) return mct_set_error(MCT_ERR_ARG, (msg));       \
+    } while (0)
+
+WarpDesc identity_desc(int rows, int cols) {
+    WarpDesc d;
+    memset(&d, 0, sizeof(d));
+    d.kind = MCT_WARP_IDENTITY;
+    d.rows = rows;
+    d.cols = cols;
+    d.hr = 0.5 * (rows - 1);
+    d.hc = 0.5 * (cols - 1);
+    return d;
+}
+
+ItemSel make_sel(const mct_items* it) {
+    ItemSel s;
+    s.gates = it->gates_dev;
+    s.epoch_ctr = it->epoch_ctr_dev;
+    s.slice_stride = it->slice_stride;
+    s.epoch_stride = it->epoch_stride;
+    s.base = it->base;
+    s.ips = it->items_per_slice;
+    s.num_slices = it->num_slices;
+    s.iteration = it->iteration;
+    s.iters_per_epoch = it->iters_per_epoch;
+    return s;
+}
+
+ItemSel single_sel(int slices) {
+    ItemSel s;
+    memset(&s, 0, sizeof(s));
+    s.ips = 1;
+    s.num_slices = slices;
+    return s;
+}
+
+int check_items(const mct_family* fam, const mct_items* it) {
+    MCT_REQUIRE(fam && it, "null family or item selector");
+    MCT_REQUIRE(it->gates_dev != nullptr, "items.gates_dev must be a device gate array");
+    MCT_REQUIRE(it->items_per_slice >= 1, "items_per_slice must be >= 1");
+    MCT_REQUIRE(it->num_slices >= 1 && it->num_slices <= fam->S,
+                "items.num_slices must lie in [1, family slices]");
+    return MCT_OK;
+}
+
+FwdArgs fwd_args(const mct_ray_plan* rp, const void* ws) {
+    FwdArgs a;
+    memset(&a, 0, sizeof(a));
+    a.ang = rp->d_fwd;
+    a.A = rp->A;
+    a.B = rp->B;
+    a.rows = rp->rows;
+    a.cols = rp->cols;
+    a.wx = rp->wx;
+    a.wxt = rp->wxt;
+    a.sp = rp->sp;
+    a.jmid = rp->jmid;
+    a.ws = static_cast<const char*>(ws);
+    a.item_bytes = rp->item_bytes;
+    a.off_x = rp->off_x;
+    a.off_xt = rp->off_xt;
+    a.off_dy = rp->off_dy;
+    a.wy = rp->wy;
+    a.pb = rp->pb;
+    return a;
+}
+
+AdjArgs adj_args(const mct_ray_plan* rp, const void* ws) {
+    AdjArgs a;
+    a.ang = rp->d_adj;
+    a.A = rp->A;
+    a.B = rp->B;
+    a.rows = rp->rows;
+    a.cols = rp->cols;
+    a.wy = rp->wy;
+    a.pb = rp->pb;
+    a.jmid = rp->jmid;
+    a.ws = static_cast<const char*>(ws);
+    a.item_bytes = rp->item_bytes;
+    a.off_dy = rp->off_dy;
+    a.off_img = rp->off_img;
+    return a;
+}
+
+PackArgs pack_args(const mct_ray_plan* rp, void* ws) {
+    PackArgs a;
+    memset(&a, 0, sizeof(a));
+    a.rows = rp->rows;
+    a.cols = rp->cols;
+    a.wx = rp->wx;
+    a.wxt = rp->wxt;
+    a.ws = static_cast<char*>(ws);
+    a.item_bytes = rp->item_bytes;
+    a.off_x = rp->off_x;
+    a.off_xt = rp->off_xt;
+    a.x_slice_stride = (long long)rp->rows * rp->cols;
+    a.cprox = 1.0f;
+    return a;
+}
+
+UpdArgs upd_args(const mct_ray_plan* rp, const void* ws) {
+    UpdArgs a;
+    memset(&a, 0, sizeof(a));
+    a.rows = rp->rows;
+    a.cols = rp->cols;
+    a.ws = static_cast<const char*>(ws);
+    a.item_bytes = rp->item_bytes;
+    a.off_img = rp->off_img;
+    return a;
+}
+}  // namespace
+
+int mct_set_error(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+extern "C" {
+
+int mct_abi_version(void) { return MCT_ABI_VERSION; }
+const char* mct_last_error(void) { return g_err.c_str(); }
+
+// ------------------------------------------------------------------ ray plan
+int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles, int num_bins,
+                        double spacing, const double* cos_a, const double* sin_a,
+                        const uint8_t* rows_dominant) {
+    MCT_REQUIRE(plan, "plan out-pointer is null");
+    *plan = nullptr;
+    // Geometry.__post_init__ (projector.py:63-68)
+    MCT_REQUIRE(rows >= 1, "rows must be >= 1");
+    MCT_REQUIRE(cols >= 1, "cols must be >= 1");
+    MCT_REQUIRE(num_angles >= 1, "num_angles must be >= 1");
+    MCT_REQUIRE(num_bins >= 1, "num_bins must be >= 1");
+    MCT_REQUIRE(spacing > 0 && isfinite(spacing), "detector_spacing must be positive");
+    MCT_REQUIRE(cos_a && sin_a && rows_dominant, "angle tables are null");
+
+    mct_ray_plan* p = new mct_ray_plan();
+    p->rows = rows;
+    p->cols = cols;
+    p->A = num_angles;
+    p->B = num_bins;
+    p->sp = spacing;
+    p->jmid = 0.5 * (num_bins - 1);
+    p->wx = cols + 2 * MCT_PADX;
+    p->wxt = rows + 2 * MCT_PADX;
+    std::vector<RayAngle> fwd(num_angles);
+    std::vector<AdjAngle> adj(num_angles);
+    const double hr = 0.5 * (rows - 1), hc = 0.5 * (cols - 1);
+    double hmax = 0.0;
+    p->has_rows = p->has_cols = 0;
+    for (int a = 0; a < num_angles; ++a) {
+        const double c = cos_a[a], s = sin_a[a];
+        RayAngle& r = fwd[a];
+        double m;
+        if (rows_dominant[a]) {
+            if (c == 0.0) {
+                delete p;
+                return mct_set_error(MCT_ERR_ARG, "rows-dominant angle with cos == 0");
+            }
+            // projector.py:137-143
+            r.P = 1.0 / c;
+            r.slope = s / c;
+            r.Q = hc - hr * r.slope;
+            m = fabs(c);
+            r.cols_dom = 0;
+            p->has_rows = 1;
+        } else {
+            if (!(s > 0.0)) {
+                delete p;
+                return mct_set_error(MCT_ERR_ARG, "cols-dominant angle with sin <= 0");
+            }
+            // projector.py:148-154
+            r.P = -1.0 / s;
+            r.slope = c / s;
+            r.Q = hr - hc * r.slope;
+            m = s;
+            r.cols_dom = 1;
+            p->has_cols = 1;
+        }
+        r.step = (float)(1.0 / m);
+        r.slope_fx = llrint(r.slope * 4294967296.0);
+        adj[a].cs = c / spacing;
+        adj[a].sn = s / spacing;
+        adj[a].step = (float)(1.0 / m);
+        adj[a].g = (float)(spacing / m);
+        hmax = std::max(hmax, m / spacing);
+    }
+    int K = std::max(0, (int)ceil(hmax - 1e-12) - 1);
+    if (K > 3) {
+        delete p;
+        return mct_set_error(MCT_ERR_ARG,
+                             "detector spacing below 1/4 pixel is not supported (adjoint footprint)");
+    }
+    p->kfoot = K;
+    const double hdiag = sqrt(hr * hr + hc * hc);
+    int pb = (int)ceil(std::max(0.0, hdiag / spacing - p->jmid)) + K + 4;
+    pb = (pb + 3) & ~3;
+    p->pb = pb;
+    p->wy = num_bins + 2 * pb;
+    size_t off = 0;
+    p->off_x = off;
+    off += align256((size_t)rows * p->wx * sizeof(float));
+    p->off_xt = off;
+    off += align256((size_t)cols * p->wxt * sizeof(float));
+    p->off_dy = off;
+    off += align256((size_t)num_angles * p->wy * sizeof(float));
+    p->off_img = off;
+    off += align256((size_t)rows * cols * sizeof(float));
+    p->item_bytes = off;
+
+    cudaError_t e = cudaMalloc(&p->d_fwd, sizeof(RayAngle) * num_angles);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_adj, sizeof(AdjAngle) * num_angles);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_fwd, fwd.data(), sizeof(RayAngle) * num_angles, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_adj, adj.data(), sizeof(AdjAngle) * num_angles, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(p->d_fwd);
+        cudaFree(p->d_adj);
+        delete p;
+        return cuda_fail(e, "mct_ray_plan_create");
+    }
+    *plan = p;
+    return MCT_OK;
+}
+
+int mct_ray_plan_destroy(mct_ray_plan* plan) {
+    if (!plan) return MCT_OK;
+    cudaFree(plan->d_fwd);
+    cudaFree(plan->d_adj);
+    delete plan;
+    return MCT_OK;
+}
+
+size_t mct_ray_workspace_bytes(const mct_ray_plan* plan, int batch) {
+    if (!plan || batch < 1) return 0;
+    return plan->item_bytes * (size_t)batch;
+}
+
+int mct_ray_forward(const mct_ray_plan* rp, const float* x, float* sino, int batch, void* ws,
+                    void* stream) {
+    MCT_REQUIRE(rp && x && sino && ws, "null argument");
+    MCT_REQUIRE(batch >= 1, "batch must be >= 1");
+    cudaStream_t st = (cudaStream_t)stream;
+    PackArgs pa = pack_args(rp, ws);
+    pa.sel = single_sel(batch);
+    pa.x = x;
+    MCT_CUDA(launch_pack(pa, batch, st), "pack");
+    FwdArgs fa = fwd_args(rp, ws);
+    fa.sel = single_sel(batch);
+    fa.out = sino;
+    fa.out_item_stride = (long long)rp->A * rp->B;
+    MCT_CUDA(launch_fwd(fa, 0, batch, st), "ray forward");
+    return MCT_OK;
+}
+
+int mct_ray_adjoint(const mct_ray_plan* rp, const float* sino, float* img, int batch, void* ws,
+                    void* stream) {
+    MCT_REQUIRE(rp && sino && img && ws, "null argument");
+    MCT_REQUIRE(batch >= 1, "batch must be >= 1");
+    cudaStream_t st = (cudaStream_t)stream;
+    MCT_CUDA(launch_pad_sino(sino, static_cast<char*>(ws), rp->item_bytes, rp->off_dy, rp->A, rp->B,
+                             rp->wy, rp->pb, batch, st),
+             "pad sinogram");
+    AdjArgs aa = adj_args(rp, ws);
+    MCT_CUDA(launch_adj(aa, rp->kfoot, batch, img, (long long)rp->rows * rp->cols, st),
+             "ray adjoint");
+    return MCT_OK;
+}
+
+// ----------------------------------------------------------------- warps
+static int warp_finish(mct_warp_plan* p, mct_warp_plan** out) {
+    cudaError_t e = cudaMalloc(&p->d_desc, sizeof(WarpDesc));
+    if (e == cudaSuccess) e = cudaMemcpy(p->d_desc, &p->desc, sizeof(WarpDesc), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(p->d_desc);
+        cudaFree(p->phi);
+        cudaFree(p->tptr);
+        cudaFree(p->tidx);
+        cudaFree(p->tw);
+        delete p;
+        return cuda_fail(e, "warp plan");
+    }
+    *out = p;
+    return MCT_OK;
+}
+
+int mct_warp_plan_create_identity(mct_warp_plan** plan, int rows, int cols) {
+    MCT_REQUIRE(plan, "plan out-pointer is null");
+    *plan = nullptr;
+    MCT_REQUIRE(rows >= 1 && cols >= 1, "invalid image shape");
+    mct_warp_plan* p = new mct_warp_plan();
+    p->desc = identity_desc(rows, cols);
+    return warp_finish(p, plan);
+}
+
+int mct_warp_plan_create_rigid(mct_warp_plan** plan, int rows, int cols, double cos_r,
+                               double sin_r, double t_row, double t_col) {
+    MCT_REQUIRE(plan, "plan out-pointer is null");
+    *plan = nullptr;
+    MCT_REQUIRE(rows >= 1 && cols >= 1, "invalid image shape");
+    MCT_REQUIRE(isfinite(cos_r) && isfinite(sin_r) && isfinite(t_row) && isfinite(t_col),
+                "motion parameters must be finite");
+    mct_warp_plan* p = new mct_warp_plan();
+    WarpDesc d = identity_desc(rows, cols);
+    d.kind = MCT_WARP_RIGID;
+    d.cs = cos_r;
+    d.sn = sin_r;
+    d.tr = t_row;
+    d.tc = t_col;
+    // inverse: p = R(theta) s + t  (motion.py:111-120 forward map T)
+    d.i00 = cos_r;
+    d.i01 = -sin_r;
+    d.i10 = sin_r;
+    d.i11 = cos_r;
+    d.o0 = t_row;
+    d.o1 = t_col;
+    d.ext0 = fabs(cos_r) + fabs(sin_r);
+    d.ext1 = d.ext0;
+    p->desc = d;
+    return warp_finish(p, plan);
+}
+
+int mct_warp_plan_create_dilatation(mct_warp_plan** plan, int rows, int cols, double scale) {
+    MCT_REQUIRE(plan, "plan out-pointer is null");
+    *plan = nullptr;
+    MCT_REQUIRE(rows >= 1 && cols >= 1, "invalid image shape");
+    MCT_REQUIRE(scale > 0 && isfinite(scale), "scale must be positive");
+    mct_warp_plan* p = new mct_warp_plan();
+    WarpDesc d = identity_desc(rows, cols);
+    d.kind = MCT_WARP_DILATATION;
+    d.scale = scale;
+    d.i00 = scale;
+    d.i11 = scale;
+    d.ext0 = scale;
+    d.ext1 = scale;
+    p->desc = d;
+    return warp_finish(p, plan);
+}
+
+int mct_warp_plan_create_dense(mct_warp_plan** plan, int rows, int cols, const float* phi_dev,
+                               void* stream) {
+    MCT_REQUIRE(plan, "plan out-pointer is null");
+    *plan = nullptr;
+    MCT_REQUIRE(rows >= 1 && cols >= 1, "invalid image shape");
+    MCT_REQUIRE(phi_dev, "phi is null");
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long n = (long long)rows * cols;
+    mct_warp_plan* p = new mct_warp_plan();
+    WarpDesc d = identity_desc(rows, cols);
+    d.kind = MCT_WARP_DENSE;
+    cudaError_t e = cudaMalloc(&p->phi, 2 * n * sizeof(float));
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(p->phi, phi_dev, 2 * n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+    // reject non-finite fields (MotionParams finiteness rule, motion.py:64-77)
+    float* d_max = nullptr;
+    float hmax = 0.0f;
+    if (e == cudaSuccess) e = cudaMalloc(&d_max, sizeof(float));
+    if (e == cudaSuccess) e = launch_absmax(p->phi, 2 * n, d_max, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hmax, d_max, sizeof(float), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d_max);
+    if (e == cudaSuccess && !isfinite(hmax)) {
+        cudaFree(p->phi);
+        delete p;
+        return mct_set_error(MCT_ERR_ARG, "displacement field must be finite");
+    }
+    if (e == cudaSuccess && hmax > 1.0e6f) {
+        cudaFree(p->phi);
+        delete p;
+        return mct_set_error(MCT_ERR_ARG, "displacement field magnitude exceeds 1e6 pixels");
+    }
+    d.phi = p->phi;
+    if (e == cudaSuccess) e = build_dense_transpose(d, &p->tptr, &p->tidx, &p->tw, &p->nnz, st);
+    if (e != cudaSuccess) {
+        cudaFree(p->phi);
+        delete p;
+        return cuda_fail(e, "mct_warp_plan_create_dense");
+    }
+    d.tptr = p->tptr;
+    d.tidx = p->tidx;
+    d.tw = p->tw;
+    p->desc = d;
+    return warp_finish(p, plan);
+}
+
+int mct_warp_plan_destroy(mct_warp_plan* plan) {
+    if (!plan) return MCT_OK;
+    cudaFree(plan->d_desc);
+    cudaFree(plan->phi);
+    cudaFree(plan->tptr);
+    cudaFree(plan->tidx);
+    cudaFree(plan->tw);
+    delete plan;
+    return MCT_OK;
+}
+
+int mct_warp_plan_kind(const mct_warp_plan* plan) { return plan ? plan->desc.kind : -1; }
+long long mct_warp_plan_nnz(const mct_warp_plan* plan) { return plan ? plan->nnz : -1; }
+
+int mct_warp_forward(const mct_warp_plan* plan, const float* x, float* out, void* stream) {
+    MCT_REQUIRE(plan && x && out, "null argument");
+    MCT_CUDA(launch_warp_fwd_plain(plan->d_desc, x, out, plan->desc.rows, plan->desc.cols,
+                                   (cudaStream_t)stream),
+             "warp forward");
+    return MCT_OK;
+}
+
+int mct_warp_adjoint(const mct_warp_plan* plan, const float* y, float* out, void* stream) {
+    MCT_REQUIRE(plan && y && out, "null argument");
+    UpdArgs a;
+    memset(&a, 0, sizeof(a));
+    a.rows = plan->desc.rows;
+    a.cols = plan->desc.cols;
+    a.img_override = y;
+    a.sel = single_sel(1);
+    a.warps = plan->d_desc;
+    a.out = out;
+    MCT_CUDA(launch_update(a, 0, 1, (cudaStream_t)stream), "warp adjoint");
+    return MCT_OK;
+}
+
+// ----------------------------------------------------------------- family
+int mct_family_create(mct_family** fam, const mct_ray_plan* ray, int num_slices, int num_gates,
+                      const mct_warp_plan* const* warps) {
+    MCT_REQUIRE(fam, "family out-pointer is null");
+    *fam = nullptr;
+    MCT_REQUIRE(ray, "ray plan is null");
+    MCT_REQUIRE(num_slices >= 1, "num_slices must be >= 1");
+    MCT_REQUIRE(num_gates >= 1, "at least one gate required");
+    std::vector<WarpDesc> descs((size_t)num_slices * num_gates);
+    for (size_t i = 0; i < descs.size(); ++i) {
+        const mct_warp_plan* w = warps ? warps[i] : nullptr;
+        if (w) {
+            if (w->desc.rows != ray->rows || w->desc.cols != ray->cols)
+                return mct_set_error(MCT_ERR_ARG, "warp shape does not match the ray geometry");
+            descs[i] = w->desc;
+        } else {
+            descs[i] = identity_desc(ray->rows, ray->cols);
+        }
+    }
+    mct_family* f = new mct_family();
+    f->ray = ray;
+    f->S = num_slices;
+    f->N = num_gates;
+    f->params_set = 0;
+    cudaError_t e = cudaMalloc(&f->d_warps, sizeof(WarpDesc) * descs.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpy(f->d_warps, descs.data(), sizeof(WarpDesc) * descs.size(),
+                       cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&f->d_params, sizeof(GateParam) * num_gates);
+    if (e == cudaSuccess) e = cudaMemset(f->d_params, 0, sizeof(GateParam) * num_gates);
+    if (e != cudaSuccess) {
+        cudaFree(f->d_warps);
+        cudaFree(f->d_params);
+        delete f;
+        return cuda_fail(e, "mct_family_create");
+    }
+    *fam = f;
+    return MCT_OK;
+}
+
+int mct_family_destroy(mct_family* fam) {
+    if (!fam) return MCT_OK;
+    cudaFree(fam->d_warps);
+    cudaFree(fam->d_params);
+    delete fam;
+    return MCT_OK;
+}
+
+int mct_family_set_params(mct_family* fam, const double* sigmas, const double* probs,
+                          double theta) {
+    MCT_REQUIRE(fam && sigmas && probs, "null argument");
+    MCT_REQUIRE(theta > 0 && theta <= 1, "theta must lie in (0, 1]");
+    std::vector<GateParam> gp(fam->N);
+    for (int g = 0; g < fam->N; ++g) {
+        MCT_REQUIRE(sigmas[g] > 0 && isfinite(sigmas[g]), "all sigmas must be positive and finite");
+        MCT_REQUIRE(probs[g] > 0 && probs[g] <= 1, "probabilities must lie in (0, 1]");
+        gp[g].sigma = (float)sigmas[g];
+        gp[g].dual_inv = (float)(1.0 / (1.0 + sigmas[g] * fam->N / 2.0));
+        gp[g].theta_over_p = (float)(theta / probs[g]);
+        gp[g].pad_ = 0.0f;
+    }
+    MCT_CUDA(cudaMemcpy(fam->d_params, gp.data(), sizeof(GateParam) * fam->N, cudaMemcpyHostToDevice),
+             "mct_family_set_params");
+    fam->params_set = 1;
+    return MCT_OK;
+}
+
+size_t mct_family_workspace_bytes(const mct_family* fam, int items) {
+    if (!fam || items < 1) return 0;
+    return fam->ray->item_bytes * (size_t)items;
+}
+
+int mct_gated_forward(const mct_family* fam, int slice, int gate, const float* x, float* sino,
+                      void* ws, void* stream) {
+    MCT_REQUIRE(fam && x && sino && ws, "null argument");
+    MCT_REQUIRE(slice >= 0 && slice < fam->S && gate >= 0 && gate < fam->N, "gate out of range");
+    const mct_ray_plan* rp = fam->ray;
+    cudaStream_t st = (cudaStream_t)stream;
+    PackArgs pa = pack_args(rp, ws);
+    pa.sel = single_sel(1);
+    pa.x = x;
+    pa.warps = fam->d_warps + (size_t)slice * fam->N + gate;
+    MCT_CUDA(launch_pack(pa, 1, st), "gated pack");
+    FwdArgs fa = fwd_args(rp, ws);
+    fa.sel = single_sel(1);
+    fa.out = sino;
+    fa.out_item_stride = (long long)rp->A * rp->B;
+    MCT_CUDA(launch_fwd(fa, 0, 1, st), "gated forward");
+    return MCT_OK;
+}
+
+int mct_gated_adjoint(const mct_family* fam, int slice, int gate, const float* y, float* img,
+                      void* ws, void* stream) {
+    MCT_REQUIRE(fam && y && img && ws, "null argument");
+    MCT_REQUIRE(slice >= 0 && slice < fam->S && gate >= 0 && gate < fam->N, "gate out of range");
+    const mct_ray_plan* rp = fam->ray;
+    cudaStream_t st = (cudaStream_t)stream;
+    MCT_CUDA(launch_pad_sino(y, static_cast<char*>(ws), rp->item_bytes, rp->off_dy, rp->A, rp->B,
+                             rp->wy, rp->pb, 1, st),
+             "pad sinogram");
+    AdjArgs aa = adj_args(rp, ws);
+    MCT_CUDA(launch_adj(aa, rp->kfoot, 1, nullptr, 0, st), "gated adjoint (A^*)");
+    UpdArgs ua = upd_args(rp, ws);
+    ua.sel = single_sel(1);
+    ua.warps = fam->d_warps + (size_t)slice * fam->N + gate;
+    ua.out = img;
+    MCT_CUDA(launch_update(ua, 0, 1, st), "gated adjoint (D^*)");
+    return MCT_OK;
+}
+
+// ------------------------------------------------------- fused iteration
+int mct_iter_prox_warp(const mct_family* fam, const mct_items* it, mct_state* s, double tau,
+                       double alpha, void* ws, void* stream) {
+    int rc = check_items(fam, it);
+    if (rc) return rc;
+    MCT_REQUIRE(s && s->x && s->zbar && s->x_next && ws, "null state buffer");
+    MCT_REQUIRE(tau >= 0 && alpha >= 0, "tau and alpha must be >= 0");
+    const mct_ray_plan* rp = fam->ray;
+    PackArgs pa = pack_args(rp, ws);
+    pa.sel = make_sel(it);
+    pa.N = fam->N;
+    pa.warps = fam->d_warps;
+    pa.x = s->x;
+    pa.zbar = s->zbar;
+    pa.tau = (float)tau;
+    pa.cprox = (float)(1.0 / (1.0 + 2.0 * alpha * tau));  // functionals.py:48
+    pa.x_next = s->x_next;
+    pa.status = s->status;
+    MCT_CUDA(launch_pack(pa, it->items_per_slice * it->num_slices, (cudaStream_t)stream),
+             "prox+warp");
+    return MCT_OK;
+}
+
+int mct_iter_forward_dual(const mct_family* fam, const mct_items* it, mct_state* s, void* ws,
+                          void* stream) {
+    int rc = check_items(fam, it);
+    if (rc) return rc;
+    MCT_REQUIRE(fam->params_set, "mct_family_set_params has not been called");
+    MCT_REQUIRE(s && s->y && s->d && ws, "null state buffer");
+    FwdArgs fa = fwd_args(fam->ray, ws);
+    fa.sel = make_sel(it);
+    fa.N = fam->N;
+    fa.y = s->y;
+    fa.d = s->d;
+    fa.proj = s->proj;
+    fa.gp = fam->d_params;
+    fa.status = s->status;
+    MCT_CUDA(launch_fwd(fa, 1, it->items_per_slice * it->num_slices, (cudaStream_t)stream),
+             "forward+dual");
+    return MCT_OK;
+}
+
+int mct_iter_adjoint(const mct_family* fam, const mct_items* it, void* ws, void* stream) {
+    int rc = check_items(fam, it);
+    if (rc) return rc;
+    MCT_REQUIRE(ws, "null workspace");
+    AdjArgs aa = adj_args(fam->ray, ws);
+    MCT_CUDA(launch_adj(aa, fam->ray->kfoot, it->items_per_slice * it->num_slices, nullptr, 0,
+                        (cudaStream_t)stream),
+             "adjoint");
+    return MCT_OK;
+}
+
+int mct_iter_adjoint_update(const mct_family* fam, const mct_items* it, mct_state* s,
+                            float* dz_partial, void* ws, void* stream) {
+    int rc = check_items(fam, it);
+    if (rc) return rc;
+    MCT_REQUIRE(fam->params_set, "mct_family_set_params has not been called");
+    MCT_REQUIRE(s && s->x && s->x_next && ws, "null state buffer");
+    UpdArgs ua = upd_args(fam->ray, ws);
+    ua.sel = make_sel(it);
+    ua.N = fam->N;
+    ua.warps = fam->d_warps;
+    ua.gp = fam->d_params;
+    ua.x = s->x;
+    ua.x_next = s->x_next;
+    int mode;
+    if (dz_partial) {
+        ua.dz = dz_partial;
+        mode = 2;
+    } else {
+        MCT_REQUIRE(s->z && s->zbar, "null z / zbar");
+        ua.z = s->z;
+        ua.zbar = s->zbar;
+        mode = 1;
+    }
+    MCT_CUDA(launch_update(ua, mode, it->num_slices, (cudaStream_t)stream), "adjoint update");
+    return MCT_OK;
+}
+
+int mct_iter_z_update(const mct_family* fam, mct_state* s, const float* dz, double theta,
+                      void* stream) {
+    MCT_REQUIRE(fam && s && s->z && s->zbar && dz, "null argument");
+    const long long n = (long long)fam->S * fam->ray->rows * fam->ray->cols;
+    MCT_CUDA(launch_z_update(n, dz, s->z, s->zbar, (float)theta, (cudaStream_t)stream), "z update");
+    return MCT_OK;
+}
+
+int mct_epoch_advance(int32_t* ctr, int32_t inc, void* stream) {
+    MCT_REQUIRE(ctr, "null counter");
+    MCT_CUDA(launch_epoch_advance(ctr, inc, (cudaStream_t)stream), "epoch advance");
+    return MCT_OK;
+}
+
+// -------------------------------------------------------------- reductions
+int mct_reduce(const float* a, const float* b, long long length, int segments, long long stride,
+               int mode, double* out, void* stream) {
+    MCT_REQUIRE(a && out, "null argument");
+    MCT_REQUIRE(length >= 0 && segments >= 1, "invalid reduction shape");
+    MCT_REQUIRE(mode == MCT_REDUCE_DOT || mode == MCT_REDUCE_SQDIFF, "invalid reduction mode");
+    MCT_CUDA(launch_reduce(a, b, length, segments, stride, mode, out, (cudaStream_t)stream), "reduce");
+    return MCT_OK;
+}
+
+int mct_axpby(long long n, float alpha, const float* x, float beta, float* y, void* stream) {
+    MCT_REQUIRE(x && y && n >= 0, "null argument");
+    MCT_CUDA(launch_axpby(n, alpha, x, beta, y, (cudaStream_t)stream), "axpby");
+    return MCT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,190 @@
+// Internal types shared by the sm_100a kernels and the C-ABI layer.
+//
+// Data layout in HBM:
+//   image x            : (rows, cols) fp32 row-major
+//   padded image X     : (rows, wx)  wx = cols + 2*PADX, column c at offset PADX + c
+//   padded transpose XT: (cols, wxt) wxt = rows + 2*PADX, row r of x at offset PADX + r
+//   padded sinogram DY : (A, wy)     wy = B + 2*pb,      bin j at offset pb + j
+// Pad regions are zero-initialised once (workspace contract) and never written,
+// so the Joseph gather loops run branch-free.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/mctomo_b200.h"
+
+#define MCT_PADX 4
+
+// ---------------------------------------------------------------- ray plan --
+// Forward (ray-driven) per-angle constants.  projector.py:134-155 restated as
+// cont(k) = P*s_j + Q + k*slope along the dominant axis k.
+struct RayAngle {
+    double P, Q, slope;
+    long long slope_fx;  // slope * 2^32 (32.32 fixed point increment)
+    float step;          // 1/max(|cos|, sin)  (projector.py:143, :154)
+    int cols_dom;        // 0: rows-dominant (sample every row), 1: cols-dominant
+};
+
+// Adjoint (pixel-driven) per-angle constants: the detector coordinate of pixel
+// centre (u, v) is jc = (v*cos - u*sin)/sp + (B-1)/2 and the Joseph weight of
+// bin j is step * max(0, 1 - |j - jc| * g) with g = sp*step (tent footprint).
+struct AdjAngle {
+    double cs, sn;  // cos/sp, sin/sp
+    float step, g;
+};
+
+struct mct_ray_plan {
+    int rows, cols, A, B;
+    double sp, jmid;     // detector spacing, (B-1)/2
+    int wx, wxt;         // padded strides (floats)
+    int pb, wy;          // sinogram pad (bins) and padded stride
+    int kfoot;           // extra footprint bins for the adjoint (0 when sp >= step^-1)
+    int has_rows, has_cols;
+    RayAngle* d_fwd;
+    AdjAngle* d_adj;
+    size_t off_x, off_xt, off_dy, off_img, item_bytes;
+};
+
+// --------------------------------------------------------------- warp plan --
+struct WarpDesc {
+    int kind;  // MCT_WARP_*
+    int rows, cols;
+    int pad_;
+    double hr, hc;           // (rows-1)/2, (cols-1)/2
+    double cs, sn, tr, tc;   // rigid
+    double scale;            // dilatation
+    // inverse map for the adjoint window: p = Minv * s + off (centred coords)
+    double i00, i01, i10, i11, o0, o1, ext0, ext1;
+    const float* phi;        // dense (2, rows, cols)
+    const int* tptr;         // dense transposed gather list (rows*cols + 1)
+    const int* tidx;
+    const float* tw;
+};
+
+struct mct_warp_plan {
+    WarpDesc desc;
+    WarpDesc* d_desc;  // device copy of desc
+    float* phi;
+    int* tptr;
+    int* tidx;
+    float* tw;
+    long long nnz;
+};
+
+// ------------------------------------------------------------------ family --
+struct GateParam {
+    float sigma, dual_inv, theta_over_p, pad_;
+};
+
+struct mct_family {
+    const mct_ray_plan* ray;
+    int S, N;
+    WarpDesc* d_warps;   // S*N descriptors
+    GateParam* d_params; // N
+    int params_set;
+};
+
+// ------------------------------------------------------------ item selector --
+struct ItemSel {
+    const int* gates;
+    const int* epoch_ctr;
+    int slice_stride, epoch_stride, base, ips, num_slices, iteration, iters_per_epoch;
+};
+
+__device__ __forceinline__ void resolve_item(const ItemSel& s, int item, int& slice, int& gate,
+                                             int& iter) {
+    slice = item / s.ips;
+    int k = item - slice * s.ips;
+    int e = s.epoch_ctr ? __ldg(s.epoch_ctr) : 0;
+    gate = s.gates ? __ldg(s.gates + (long long)slice * s.slice_stride +
+                           (long long)e * s.epoch_stride + s.base + k)
+                   : 0;
+    iter = s.epoch_ctr ? e * s.iters_per_epoch + s.iteration : s.iteration;
+}
+
+// ------------------------------------------------------------ kernel args --
+struct PackArgs {
+    int rows, cols, wx, wxt;
+    char* ws;
+    size_t item_bytes, off_x, off_xt;
+    ItemSel sel;
+    int N;
+    const WarpDesc* warps;   // NULL: identity; with sel.gates NULL: warps[0]
+    const float* x;          // (slices, rows, cols)
+    long long x_slice_stride;
+    const float* zbar;       // prox mode when non-NULL
+    float tau, cprox;
+    float* x_next;           // written by item k==0 of each slice in prox mode
+    unsigned long long* status;
+};
+
+struct FwdArgs {
+    const RayAngle* ang;
+    int A, B, rows, cols, wx, wxt;
+    double sp, jmid;
+    const char* ws;
+    size_t item_bytes, off_x, off_xt, off_dy;
+    int wy, pb;
+    ItemSel sel;
+    int N;
+    // plain epilogue
+    float* out;
+    long long out_item_stride;
+    // dual epilogue
+    float* y;
+    const float* d;
+    float* proj;
+    const GateParam* gp;
+    unsigned long long* status;
+};
+
+struct AdjArgs {
+    const AdjAngle* ang;
+    int A, B, rows, cols, wy, pb;
+    double jmid;
+    const char* ws;
+    size_t item_bytes, off_dy, off_img;
+};
+
+struct UpdArgs {
+    int rows, cols;
+    const char* ws;
+    size_t item_bytes, off_img;
+    const float* img_override;  // plain D^* of a caller image (single item)
+    ItemSel sel;
+    int N;
+    const WarpDesc* warps;
+    const GateParam* gp;
+    float* out;       // mode 0
+    float* z;         // mode 1
+    float* zbar;
+    float* x;
+    const float* x_next;
+    float* dz;        // mode 2
+};
+
+// ------------------------------------------------------------- launchers --
+cudaError_t launch_pack(const PackArgs& a, int items, cudaStream_t st);
+cudaError_t launch_pad_sino(const float* sino, char* ws, size_t item_bytes, size_t off_dy, int A,
+                            int B, int wy, int pb, int items, cudaStream_t st);
+cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st);
+cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, float* out,
+                       long long out_item_stride, cudaStream_t st);
+cudaError_t launch_update(const UpdArgs& a, int mode, int slices, cudaStream_t st);
+cudaError_t launch_z_update(long long n, const float* dz, float* z, float* zbar, float theta,
+                            cudaStream_t st);
+cudaError_t launch_epoch_advance(int* ctr, int inc, cudaStream_t st);
+cudaError_t launch_warp_fwd_plain(const WarpDesc* d_desc, const float* x, float* out, int rows,
+                                  int cols, cudaStream_t st);
+cudaError_t launch_reduce(const float* a, const float* b, long long len, int segs,
+                          long long stride, int mode, double* out, cudaStream_t st);
+cudaError_t launch_axpby(long long n, float alpha, const float* x, float beta, float* y,
+                         cudaStream_t st);
+cudaError_t launch_absmax(const float* x, long long n, float* out, cudaStream_t st);
+cudaError_t build_dense_transpose(const WarpDesc& desc, int** tptr, int** tidx, float** tw,
+                                  long long* nnz, cudaStream_t st);
+
+// error reporting (abi.cu)
+int mct_set_error(int code, const std::string& msg);

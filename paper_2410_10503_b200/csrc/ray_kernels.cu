@@ -1,0 +1,312 @@
+// sm_100a kernels of the hot path: fused prox+warp+pack, Joseph forward with
+// fused dual prox, pixel-driven transpose-gather adjoint.
+//
+// Reference: projector.py:126-217 (Joseph traversal tables, gather/scatter),
+// motion.py:132-183 (warp), functionals.py:40-68 (proxes), solvers.py:316-366.
+#include "mct_internal.cuh"
+#include "warp_math.cuh"
+
+#include <math.h>
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// K1 / pack: W = D_g(x_new), x_new = prox_g(x - tau*zbar) (or x_new = x), written
+// into the padded row-major X and padded transposed XT of the item workspace.
+// Tile 32x32, block 32x8, transposed store staged through shared memory.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) pack_kernel(PackArgs p) {
+    __shared__ float tile[32][33];
+    const int item = blockIdx.z;
+    int slice, gate, iter;
+    resolve_item(p.sel, item, slice, gate, iter);
+    const int k_in_slice = item - slice * p.sel.ips;
+    const float* __restrict__ x = p.x + (long long)slice * p.x_slice_stride;
+    const float* __restrict__ zb = p.zbar ? p.zbar + (long long)slice * p.x_slice_stride : nullptr;
+    const bool prox = (zb != nullptr);
+    const float tau = p.tau, cp = p.cprox;
+    const int rows = p.rows, cols = p.cols;
+
+    WarpDesc wd;
+    bool ident = (p.warps == nullptr);
+    if (!ident) {
+        wd = p.warps[p.sel.gates ? (long long)slice * p.N + gate : 0];
+        ident = (wd.kind == MCT_WARP_IDENTITY);
+    }
+
+    auto xnew = [&](int rr, int cc) -> float {
+        long long o = (long long)rr * cols + cc;
+        float v = __ldg(x + o);
+        if (prox) v = (v - tau * __ldg(zb + o)) * cp;
+        return v;
+    };
+
+    char* base = p.ws + (size_t)item * p.item_bytes;
+    float* X = reinterpret_cast<float*>(base + p.off_x);
+    float* XT = reinterpret_cast<float*>(base + p.off_xt);
+
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const bool writer = prox && k_in_slice == 0 && p.x_next != nullptr;
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        int r = r0 + ty + 8 * k, c = c0 + tx;
+        float w = 0.0f;
+        if (r < rows && c < cols) {
+            if (ident) {
+                w = xnew(r, c);
+            } else {
+                w = warp_apply_at(wd, r, c, xnew);
+            }
+            X[(long long)r * p.wx + MCT_PADX + c] = w;
+            if (writer) {
+                float xn = xnew(r, c);
+                p.x_next[(long long)slice * p.x_slice_stride + (long long)r * cols + c] = xn;
+                bad |= !isfinite(xn);
+            }
+        }
+        tile[ty + 8 * k][tx] = w;
+    }
+    if (writer && p.status && __any_sync(0xffffffffu, bad)) {
+        if ((threadIdx.x & 31) == 0) atomicMin(p.status, (unsigned long long)iter);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        int c = c0 + ty + 8 * k, r = r0 + tx;
+        if (r < rows && c < cols) XT[(long long)c * p.wxt + MCT_PADX + r] = tile[tx][ty + 8 * k];
+    }
+}
+
+// Copy a plain (A, B) sinogram into the padded DY layout of each item.
+__global__ void pad_sino_kernel(const float* __restrict__ sino, char* ws, size_t item_bytes,
+                                size_t off_dy, int A, int B, int wy, int pb) {
+    const int item = blockIdx.z;
+    const int a = blockIdx.y;
+    float* DY = reinterpret_cast<float*>(ws + (size_t)item * item_bytes + off_dy);
+    const float* s = sino + ((long long)item * A + a) * B;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x)
+        DY[(long long)a * wy + pb + j] = s[j];
+}
+
+// ---------------------------------------------------------------------------
+// K2: Joseph forward A (projector.py:201-207 with the weights of :160-183).
+// Block = 8 warps = 8 consecutive angles x 32 consecutive bins: the warps walk
+// nearly the same image lines so most of the 2 taps per sample hit L1.
+// Along the dominant axis the continuous minor index advances by a constant
+// slope; it is carried in 32.32 fixed point (integer part = tap index, fraction
+// = interpolation weight), anchored on a per-ray fp64 start, so no float
+// conversions sit in the inner loop.  Rows that cannot contribute are skipped
+// analytically; the padded layout keeps the loop branch-free.
+// MODE 0: plain store.  MODE 1: fused dual prox (functionals.py:53-68,
+// solvers.py:341-357) writing y, dy (padded, for K3) and optionally proj.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float frac_from_fx(unsigned lo) {
+    return __uint_as_float(0x3f800000u | (lo >> 9)) - 1.0f;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) fwd_kernel(FwdArgs p) {
+    const int item = blockIdx.z;
+    const int a = blockIdx.y * 8 + threadIdx.y;
+    const int j = blockIdx.x * 32 + threadIdx.x;
+    if (a >= p.A) return;
+    const bool active = j < p.B;
+    const RayAngle ra = p.ang[a];
+    const char* base = p.ws + (size_t)item * p.item_bytes;
+    const int cd = ra.cols_dom;
+    const float* __restrict__ X =
+        reinterpret_cast<const float*>(base + (cd ? p.off_xt : p.off_x)) + MCT_PADX;
+    const int stride = cd ? p.wxt : p.wx;
+    const int nmaj = cd ? p.cols : p.rows;
+    const int lim = cd ? p.rows : p.cols;
+
+    float acc = 0.0f;
+    if (active) {
+        const double sj = ((double)j - p.jmid) * p.sp;
+        const double c0 = ra.P * sj + ra.Q;
+        int lo, hi;
+        if (ra.slope == 0.0) {
+            if (c0 > -1.0 && c0 < (double)lim) { lo = 0; hi = nmaj - 1; }
+            else { lo = 0; hi = -1; }
+        } else {
+            double ka = (-1.0 - c0) / ra.slope, kb = ((double)lim - c0) / ra.slope;
+            const double top = (double)nmaj + 2.0;
+            double kmin = fmin(fmax(fmin(ka, kb), -2.0), top);
+            double kmax = fmin(fmax(fmax(ka, kb), -2.0), top);
+            lo = max(0, (int)floor(kmin));
+            hi = min(nmaj - 1, (int)ceil(kmax));
+        }
+        if (lo <= hi) {
+            long long fx = __double2ll_rn((c0 + (double)lo * ra.slope) * 4294967296.0);
+            const long long sfx = ra.slope_fx;
+            const float* row = X + (long long)lo * stride;
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+            int k = lo;
+            for (; k + 3 <= hi; k += 4) {
+                const long long f1 = fx + sfx, f2 = f1 + sfx, f3 = f2 + sfx;
+                const float* q0 = row + (int)(fx >> 32);
+                const float* q1 = row + stride + (int)(f1 >> 32);
+                const float* q2 = row + 2 * stride + (int)(f2 >> 32);
+                const float* q3 = row + 3 * stride + (int)(f3 >> 32);
+                float v00 = __ldg(q0), v01 = __ldg(q0 + 1);
+                float v10 = __ldg(q1), v11 = __ldg(q1 + 1);
+                float v20 = __ldg(q2), v21 = __ldg(q2 + 1);
+                float v30 = __ldg(q3), v31 = __ldg(q3 + 1);
+                a0 += fmaf(frac_from_fx((unsigned)fx), v01 - v00, v00);
+                a1 += fmaf(frac_from_fx((unsigned)f1), v11 - v10, v10);
+                a2 += fmaf(frac_from_fx((unsigned)f2), v21 - v20, v20);
+                a3 += fmaf(frac_from_fx((unsigned)f3), v31 - v30, v30);
+                fx = f3 + sfx;
+                row += 4 * stride;
+            }
+            for (; k <= hi; ++k) {
+                const float* q0 = row + (int)(fx >> 32);
+                float v00 = __ldg(q0), v01 = __ldg(q0 + 1);
+                a0 += fmaf(frac_from_fx((unsigned)fx), v01 - v00, v00);
+                fx += sfx;
+                row += stride;
+            }
+            acc = (a0 + a1) + (a2 + a3);
+        }
+    }
+    const float proj = acc * ra.step;
+    if (!active) return;
+    if (MODE == 0) {
+        p.out[(long long)item * p.out_item_stride + (long long)a * p.B + j] = proj;
+    } else {
+        int slice, gate, iter;
+        resolve_item(p.sel, item, slice, gate, iter);
+        const long long off = (((long long)slice * p.N + gate) * p.A + a) * p.B + j;
+        const GateParam gp = p.gp[gate];
+        const float yv = p.y[off];
+        const float dv = __ldg(p.d + off);
+        const float yn = (fmaf(gp.sigma, proj, yv) - gp.sigma * dv) * gp.dual_inv;
+        p.y[off] = yn;
+        float* DY = reinterpret_cast<float*>(const_cast<char*>(base) + p.off_dy);
+        DY[(long long)a * p.wy + p.pb + j] = yn - yv;
+        if (p.proj) p.proj[off] = proj;
+        if (!isfinite(yn) && p.status)
+            atomicMin(p.status + 1, ((unsigned long long)iter << 20) | (unsigned long long)gate);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: A^* as a deterministic transpose-gather (no atomics).  Pixel (r, c) at
+// angle a receives  step * max(0, 1 - |j - jc|*g) * dy[a, j]  from the bins j
+// around its detector coordinate jc — exactly the Joseph weight of
+// projector.py:161-166 seen from the pixel (the tent identity pinned by
+// test_projector.py:78-93).  jc is anchored per 16x16 tile and angle in fp64
+// (integer bin + fp32 fraction) and offset per pixel in fp32, which keeps the
+// coordinate error ~1e-6 bins at 1024^2.
+// ---------------------------------------------------------------------------
+#define ADJ_TILE 16
+#define ADJ_CH 256
+#define MAGIC_F 12582912.0f  // 1.5 * 2^23
+#define MAGIC_I 0x4B400000
+
+template <int K>
+__global__ void __launch_bounds__(256) adj_kernel(AdjArgs p, float* out, long long out_stride) {
+    __shared__ float4 s_a[ADJ_CH];  // f0 - 0.5, cos/sp, sin/sp, step*g
+    __shared__ float4 s_b[ADJ_CH];  // step, step - step*g, row offset (int bits), -
+    const int item = blockIdx.z;
+    const int tid = threadIdx.y * ADJ_TILE + threadIdx.x;
+    const int r0 = blockIdx.y * ADJ_TILE, c0 = blockIdx.x * ADJ_TILE;
+    const int r = r0 + threadIdx.y, c = c0 + threadIdx.x;
+    const bool inside = (r < p.rows) && (c < p.cols);
+    const double u0 = (double)r0 + 7.5 - 0.5 * (double)(p.rows - 1);
+    const double v0 = (double)c0 + 7.5 - 0.5 * (double)(p.cols - 1);
+    const float du = (float)threadIdx.y - 7.5f, dv = (float)threadIdx.x - 7.5f;
+    const char* base = p.ws + (size_t)item * p.item_bytes;
+    const float* __restrict__ DY = reinterpret_cast<const float*>(base + p.off_dy);
+
+    float acc0 = 0.0f, acc1 = 0.0f;
+    for (int a0 = 0; a0 < p.A; a0 += ADJ_CH) {
+        const int cnt = min(ADJ_CH, p.A - a0);
+        __syncthreads();
+        if (tid < cnt) {
+            const AdjAngle aa = p.ang[a0 + tid];
+            const double jc = v0 * aa.cs - u0 * aa.sn + p.jmid;
+            const double J = floor(jc);
+            const float f0 = (float)(jc - J);
+            const float gs = aa.step * aa.g;
+            s_a[tid] = make_float4(f0 - 0.5f, (float)aa.cs, (float)aa.sn, gs);
+            s_b[tid] = make_float4(aa.step, aa.step - gs,
+                                   __int_as_float((a0 + tid) * p.wy + p.pb + (int)J), 0.0f);
+        }
+        __syncthreads();
+        if (inside) {
+#pragma unroll 2
+            for (int t = 0; t < cnt; ++t) {
+                const float4 A4 = s_a[t];
+                const float4 B4 = s_b[t];
+                const float tm = fmaf(dv, A4.y, fmaf(-du, A4.z, A4.x));  // jc - J - 0.5
+                const float tb = tm + MAGIC_F;
+                const int kf = __float_as_int(tb) - MAGIC_I;              // ~floor(jc - J)
+                const float d = (tm - (tb - MAGIC_F)) + 0.5f;            // jc - J - kf
+                const float* q = DY + (__float_as_int(B4.z) + kf);
+                if (K == 0) {
+                    const float w0 = fmaxf(0.0f, fmaf(-d, A4.w, B4.x));
+                    const float w1 = fmaxf(0.0f, fmaf(d, A4.w, B4.y));
+                    acc0 = fmaf(w0, __ldg(q), acc0);
+                    acc1 = fmaf(w1, __ldg(q + 1), acc1);
+                } else {
+#pragma unroll
+                    for (int m = -K; m <= K + 1; ++m) {
+                        const float dist = fabsf((float)m - d);
+                        const float w = fmaxf(0.0f, fmaf(-dist, A4.w, B4.x));
+                        acc0 = fmaf(w, __ldg(q + m), acc0);
+                    }
+                }
+            }
+        }
+    }
+    if (inside) {
+        const float v = acc0 + acc1;
+        if (out) {
+            out[(long long)item * out_stride + (long long)r * p.cols + c] = v;
+        } else {
+            float* IMG = reinterpret_cast<float*>(const_cast<char*>(base) + p.off_img);
+            IMG[(long long)r * p.cols + c] = v;
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_pack(const PackArgs& a, int items, cudaStream_t st) {
+    dim3 block(32, 8), grid((a.cols + 31) / 32, (a.rows + 31) / 32, items);
+    pack_kernel<<<grid, block, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pad_sino(const float* sino, char* ws, size_t item_bytes, size_t off_dy, int A,
+                            int B, int wy, int pb, int items, cudaStream_t st) {
+    dim3 block(256), grid((B + 255) / 256, A, items);
+    pad_sino_kernel<<<grid, block, 0, st>>>(sino, ws, item_bytes, off_dy, A, B, wy, pb);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st) {
+    dim3 block(32, 8), grid((a.B + 31) / 32, (a.A + 7) / 8, items);
+    if (mode == 0)
+        fwd_kernel<0><<<grid, block, 0, st>>>(a);
+    else
+        fwd_kernel<1><<<grid, block, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, float* out,
+                       long long out_item_stride, cudaStream_t st) {
+    dim3 block(ADJ_TILE, ADJ_TILE),
+        grid((a.cols + ADJ_TILE - 1) / ADJ_TILE, (a.rows + ADJ_TILE - 1) / ADJ_TILE, items);
+    switch (kfoot) {
+        case 0: adj_kernel<0><<<grid, block, 0, st>>>(a, out, out_item_stride); break;
+        case 1: adj_kernel<1><<<grid, block, 0, st>>>(a, out, out_item_stride); break;
+        case 2: adj_kernel<2><<<grid, block, 0, st>>>(a, out, out_item_stride); break;
+        case 3: adj_kernel<3><<<grid, block, 0, st>>>(a, out, out_item_stride); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}

@@ -1,0 +1,292 @@
+// sm_100a kernels: warp adjoint fused with the z / zbar / x update (K4), the
+// standalone warp forward, the dense-field transpose build, reductions.
+//
+// Reference: motion.py:178-194 (D, D^*), solvers.py:358-363 (z, zbar, x updates),
+// linops.py:262-263 / functionals.py:71-82 (inner products).
+#include "mct_internal.cuh"
+#include "warp_math.cuh"
+
+#include <cub/cub.cuh>
+
+namespace {
+
+// K4 — one thread per pixel q of one slice (blockIdx.y): sums D_g^* img_k over
+// the slice's items in a fixed order (deterministic), then
+//   mode 0: out = sum                       (standalone D^* / gated adjoint)
+//   mode 1: z += sum; zbar = z + sum_k (theta/p_k) D^*img_k; x = x_next
+//   mode 2: dz = sum; x = x_next            (gate-sharded PDHG partial)
+template <int MODE>
+__global__ void __launch_bounds__(256) update_kernel(UpdArgs p) {
+    const int slice = blockIdx.y;
+    const long long n = (long long)p.rows * p.cols;
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int qr = (int)(q / p.cols), qc = (int)(q - (long long)qr * p.cols);
+    float sum = 0.0f, wsum = 0.0f;
+    for (int k = 0; k < p.sel.ips; ++k) {
+        const int item = slice * p.sel.ips + k;
+        int s_, gate, iter;
+        resolve_item(p.sel, item, s_, gate, iter);
+        const float* img = p.img_override
+                               ? p.img_override
+                               : reinterpret_cast<const float*>(p.ws + (size_t)item * p.item_bytes +
+                                                                p.off_img);
+        float v;
+        if (p.warps == nullptr) {
+            v = __ldg(img + q);
+        } else {
+            const WarpDesc& wd = p.warps[p.sel.gates ? (long long)slice * p.N + gate : 0];
+            v = warp_adjoint_at(wd, img, qr, qc);
+        }
+        sum += v;
+        if (MODE == 1) wsum = fmaf(p.gp[gate].theta_over_p, v, wsum);
+    }
+    const long long o = (long long)slice * n + q;
+    if (MODE == 0) {
+        p.out[o] = sum;
+    } else if (MODE == 1) {
+        const float zq = p.z[o] + sum;
+        p.z[o] = zq;
+        p.zbar[o] = zq + wsum;
+        p.x[o] = p.x_next[o];
+    } else {
+        p.dz[o] = sum;
+        p.x[o] = p.x_next[o];
+    }
+}
+
+__global__ void z_update_kernel(long long n, const float* __restrict__ dz, float* z, float* zbar,
+                                float theta) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float d = dz[i];
+        const float zq = z[i] + d;
+        z[i] = zq;
+        zbar[i] = fmaf(theta, d, zq);
+    }
+}
+
+__global__ void epoch_advance_kernel(int* ctr, int inc) { *ctr += inc; }
+
+__global__ void warp_fwd_plain_kernel(const WarpDesc* __restrict__ desc, const float* __restrict__ x,
+                                      float* out, int rows, int cols) {
+    const long long n = (long long)rows * cols;
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const WarpDesc wd = *desc;
+    const int r = (int)(q / cols), c = (int)(q - (long long)r * cols);
+    if (wd.kind == MCT_WARP_IDENTITY) {
+        out[q] = x[q];
+        return;
+    }
+    out[q] = warp_apply_at(wd, r, c,
+                           [&](int rr, int cc) { return __ldg(x + (long long)rr * cols + cc); });
+}
+
+// ------------------------------------------------- dense transpose build --
+__global__ void dense_count_kernel(WarpDesc wd, int* cnt) {
+    const long long n = (long long)wd.rows * wd.cols;
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int r = (int)(p / wd.cols), c = (int)(p - (long long)r * wd.cols);
+    TapSet t = warp_taps(wd, r, c);
+    for (int dr = 0; dr < 2; ++dr)
+        for (int dc = 0; dc < 2; ++dc) {
+            int rr = t.r0 + dr, cc = t.c0 + dc;
+            if (rr >= 0 && rr < wd.rows && cc >= 0 && cc < wd.cols && tap_weight(t, dr, dc) != 0.0f)
+                atomicAdd(cnt + (long long)rr * wd.cols + cc, 1);
+        }
+}
+
+__global__ void dense_fill_kernel(WarpDesc wd, int* cursor, int* tidx, float* tw) {
+    const long long n = (long long)wd.rows * wd.cols;
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int r = (int)(p / wd.cols), c = (int)(p - (long long)r * wd.cols);
+    TapSet t = warp_taps(wd, r, c);
+    for (int dr = 0; dr < 2; ++dr)
+        for (int dc = 0; dc < 2; ++dc) {
+            int rr = t.r0 + dr, cc = t.c0 + dc;
+            float w = tap_weight(t, dr, dc);
+            if (rr >= 0 && rr < wd.rows && cc >= 0 && cc < wd.cols && w != 0.0f) {
+                int pos = atomicAdd(cursor + (long long)rr * wd.cols + cc, 1);
+                tidx[pos] = (int)p;
+                tw[pos] = w;
+            }
+        }
+}
+
+// Sort each (short) segment by source pixel so the gather order — and hence the
+// fp32 sum — is independent of atomic arrival order.
+__global__ void dense_sort_kernel(long long n, const int* tptr, int* tidx, float* tw) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int e0 = tptr[q], e1 = tptr[q + 1];
+    for (int i = e0 + 1; i < e1; ++i) {
+        int key = tidx[i];
+        float w = tw[i];
+        int k = i - 1;
+        while (k >= e0 && tidx[k] > key) {
+            tidx[k + 1] = tidx[k];
+            tw[k + 1] = tw[k];
+            --k;
+        }
+        tidx[k + 1] = key;
+        tw[k + 1] = w;
+    }
+}
+
+// ------------------------------------------------------------ reductions --
+// One block per segment, fixed thread->element map and fixed tree: the fp64
+// result is bitwise reproducible run to run.
+__global__ void __launch_bounds__(512) reduce_kernel(const float* __restrict__ a,
+                                                     const float* __restrict__ b, long long len,
+                                                     long long stride, int mode, double* out) {
+    __shared__ double sh[512];
+    const int s = blockIdx.x;
+    const float* as = a + (long long)s * stride;
+    const float* bs = b ? b + (long long)s * stride : nullptr;
+    double acc = 0.0;
+    for (long long i = threadIdx.x; i < len; i += blockDim.x) {
+        double x = (double)as[i];
+        if (mode == MCT_REDUCE_DOT) {
+            acc += x * (double)(bs ? bs[i] : 1.0f);
+        } else {
+            double d = bs ? x - (double)bs[i] : x;
+            acc += d * d;
+        }
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[s] = sh[0];
+}
+
+__global__ void axpby_kernel(long long n, float alpha, const float* __restrict__ x, float beta,
+                             float* y) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        y[i] = fmaf(alpha, x[i], beta * y[i]);
+}
+
+__global__ void absmax_kernel(const float* __restrict__ x, long long n, float* out) {
+    __shared__ float sh[256];
+    float m = 0.0f;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) m = fmaxf(m, fabsf(x[i]));
+    sh[threadIdx.x] = m;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] = fmaxf(sh[threadIdx.x], sh[threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+inline int grid_for(long long n, int block) {
+    long long g = (n + block - 1) / block;
+    if (g > 148LL * 32) g = 148LL * 32;
+    return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+cudaError_t launch_update(const UpdArgs& a, int mode, int slices, cudaStream_t st) {
+    const long long n = (long long)a.rows * a.cols;
+    dim3 block(256), grid((unsigned)((n + 255) / 256), slices);
+    switch (mode) {
+        case 0: update_kernel<0><<<grid, block, 0, st>>>(a); break;
+        case 1: update_kernel<1><<<grid, block, 0, st>>>(a); break;
+        case 2: update_kernel<2><<<grid, block, 0, st>>>(a); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_z_update(long long n, const float* dz, float* z, float* zbar, float theta,
+                            cudaStream_t st) {
+    z_update_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, dz, z, zbar, theta);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_epoch_advance(int* ctr, int inc, cudaStream_t st) {
+    epoch_advance_kernel<<<1, 1, 0, st>>>(ctr, inc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_warp_fwd_plain(const WarpDesc* d_desc, const float* x, float* out, int rows,
+                                  int cols, cudaStream_t st) {
+    const long long n = (long long)rows * cols;
+    warp_fwd_plain_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_desc, x, out, rows, cols);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce(const float* a, const float* b, long long len, int segs, long long stride,
+                          int mode, double* out, cudaStream_t st) {
+    reduce_kernel<<<segs, 512, 0, st>>>(a, b, len, stride, mode, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_axpby(long long n, float alpha, const float* x, float beta, float* y,
+                         cudaStream_t st) {
+    axpby_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, alpha, x, beta, y);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_absmax(const float* x, long long n, float* out, cudaStream_t st) {
+    absmax_kernel<<<1, 256, 0, st>>>(x, n, out);
+    return cudaGetLastError();
+}
+
+// Synchronous (plan construction only).
+cudaError_t build_dense_transpose(const WarpDesc& desc, int** tptr_out, int** tidx_out,
+                                  float** tw_out, long long* nnz_out, cudaStream_t st) {
+    const long long n = (long long)desc.rows * desc.cols;
+    int *cnt = nullptr, *tptr = nullptr, *tidx = nullptr;
+    float* tw = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    int total = 0;
+    cudaError_t e;
+    const unsigned nb = (unsigned)((n + 255) / 256);
+#define CK(x)              \
+    do {                   \
+        e = (x);           \
+        if (e != cudaSuccess) goto fail; \
+    } while (0)
+    CK(cudaMalloc(&cnt, (n + 1) * sizeof(int)));
+    CK(cudaMalloc(&tptr, (n + 1) * sizeof(int)));
+    CK(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(int), st));
+    dense_count_kernel<<<nb, 256, 0, st>>>(desc, cnt);
+    CK(cudaGetLastError());
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, tptr, (int)(n + 1), st));
+    CK(cudaMalloc(&tmp, tmp_bytes));
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, tptr, (int)(n + 1), st));
+    CK(cudaMemcpyAsync(&total, tptr + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMalloc(&tidx, (size_t)(total > 0 ? total : 1) * sizeof(int)));
+    CK(cudaMalloc(&tw, (size_t)(total > 0 ? total : 1) * sizeof(float)));
+    CK(cudaMemcpyAsync(cnt, tptr, n * sizeof(int), cudaMemcpyDeviceToDevice, st));
+    dense_fill_kernel<<<nb, 256, 0, st>>>(desc, cnt, tidx, tw);
+    CK(cudaGetLastError());
+    dense_sort_kernel<<<nb, 256, 0, st>>>(n, tptr, tidx, tw);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    cudaFree(cnt);
+    cudaFree(tmp);
+    *tptr_out = tptr;
+    *tidx_out = tidx;
+    *tw_out = tw;
+    *nnz_out = total;
+    return cudaSuccess;
+fail:
+    cudaFree(cnt);
+    cudaFree(tmp);
+    cudaFree(tptr);
+    cudaFree(tidx);
+    cudaFree(tw);
+    return e;
+#undef CK
+}

@@ -1,0 +1,121 @@
+// Bilinear inverse-mapping warp D (motion.py:132-183) and its transpose
+// (motion.py:185-194), restated as per-pixel device functions.
+//
+// The forward computes the source position of output pixel p and its four
+// bilinear taps; the adjoint enumerates the output pixels p whose taps contain
+// q and re-evaluates *the same* function, so forward and adjoint weights are
+// bit-identical (the pair is an exact transpose up to summation order).
+#pragma once
+
+#include "mct_internal.cuh"
+
+struct TapSet {
+    int r0, c0;
+    float fr, fc;
+};
+
+// Source position of output pixel (r, c).
+//  rigid      : motion.py:139-151 (snapped cos/sin supplied by the host),
+//               du = u - t_r; dv = v - t_c; su = cos*du + sin*dv; sv = -sin*du + cos*dv
+//  dilatation : motion.py:152-154, su = u/scale, sv = v/scale
+//  dense      : src = (r + phi_r, c + phi_c); integer part taken from phi alone so
+//               the index is exact in fp32
+// The _rn intrinsics forbid FMA contraction so the rigid/dilatation source
+// coordinates round exactly like numpy's separate multiply and add.
+__device__ __forceinline__ TapSet warp_taps(const WarpDesc& w, int r, int c) {
+    TapSet t;
+    if (w.kind == MCT_WARP_DENSE) {
+        const long long n = (long long)w.rows * w.cols;
+        const long long p = (long long)r * w.cols + c;
+        float pr = __ldg(w.phi + p);
+        float pc = __ldg(w.phi + n + p);
+        float flr = floorf(pr), flc = floorf(pc);
+        t.r0 = r + (int)flr;
+        t.c0 = c + (int)flc;
+        t.fr = pr - flr;
+        t.fc = pc - flc;
+        return t;
+    }
+    double u = __dsub_rn((double)r, w.hr);
+    double v = __dsub_rn((double)c, w.hc);
+    double su, sv;
+    if (w.kind == MCT_WARP_RIGID) {
+        double du = __dsub_rn(u, w.tr);
+        double dv = __dsub_rn(v, w.tc);
+        su = __dadd_rn(__dmul_rn(w.cs, du), __dmul_rn(w.sn, dv));
+        sv = __dadd_rn(__dmul_rn(-w.sn, du), __dmul_rn(w.cs, dv));
+    } else {  // dilatation
+        su = __ddiv_rn(u, w.scale);
+        sv = __ddiv_rn(v, w.scale);
+    }
+    double sr = __dadd_rn(su, w.hr);
+    double sc = __dadd_rn(sv, w.hc);
+    double fr0 = floor(sr), fc0 = floor(sc);
+    // clamp before int conversion (far out-of-frame translations)
+    fr0 = fmin(fmax(fr0, -4.0), (double)w.rows + 4.0);
+    fc0 = fmin(fmax(fc0, -4.0), (double)w.cols + 4.0);
+    t.r0 = (int)fr0;
+    t.c0 = (int)fc0;
+    t.fr = (float)__dsub_rn(sr, floor(sr));
+    t.fc = (float)__dsub_rn(sc, floor(sc));
+    return t;
+}
+
+// Weight of tap (dr, dc) in {0,1}^2 — motion.py:157-161 ordering.
+__device__ __forceinline__ float tap_weight(const TapSet& t, int dr, int dc) {
+    float wr = dr ? t.fr : (1.0f - t.fr);
+    float wc = dc ? t.fc : (1.0f - t.fc);
+    return wr * wc;
+}
+
+// Forward warp value at output pixel (r, c) reading input through `fetch(tr, tc)`
+// (only called for in-grid taps).
+template <typename Fetch>
+__device__ __forceinline__ float warp_apply_at(const WarpDesc& w, int r, int c, Fetch fetch) {
+    TapSet t = warp_taps(w, r, c);
+    float acc = 0.0f;
+#pragma unroll
+    for (int dr = 0; dr < 2; ++dr) {
+#pragma unroll
+        for (int dc = 0; dc < 2; ++dc) {
+            int rr = t.r0 + dr, cc = t.c0 + dc;
+            if (rr >= 0 && rr < w.rows && cc >= 0 && cc < w.cols) {
+                acc = fmaf(tap_weight(t, dr, dc), fetch(rr, cc), acc);
+            }
+        }
+    }
+    return acc;
+}
+
+// Transpose at pixel q = (qr, qc): sum over output pixels p with q among taps(p)
+// of w(p, q) * y[p].  Deterministic gather (fixed candidate order).
+__device__ __forceinline__ float warp_adjoint_at(const WarpDesc& w, const float* __restrict__ y,
+                                                 int qr, int qc) {
+    if (w.kind == MCT_WARP_IDENTITY) return __ldg(y + (long long)qr * w.cols + qc);
+    if (w.kind == MCT_WARP_DENSE) {
+        const long long q = (long long)qr * w.cols + qc;
+        int e0 = __ldg(w.tptr + q), e1 = __ldg(w.tptr + q + 1);
+        float acc = 0.0f;
+        for (int e = e0; e < e1; ++e) acc = fmaf(__ldg(w.tw + e), __ldg(y + __ldg(w.tidx + e)), acc);
+        return acc;
+    }
+    // affine: candidates p in the bounding box of T([q-1, q+1]^2)
+    double uq = (double)qr - w.hr, vq = (double)qc - w.hc;
+    double cu = w.i00 * uq + w.i01 * vq + w.o0 + w.hr;
+    double cv = w.i10 * uq + w.i11 * vq + w.o1 + w.hc;
+    int rlo = max(0, (int)floor(fmax(cu - w.ext0, -2.0)) - 1);
+    int rhi = min(w.rows - 1, (int)ceil(fmin(cu + w.ext0, (double)w.rows + 2.0)) + 1);
+    int clo = max(0, (int)floor(fmax(cv - w.ext1, -2.0)) - 1);
+    int chi = min(w.cols - 1, (int)ceil(fmin(cv + w.ext1, (double)w.cols + 2.0)) + 1);
+    float acc = 0.0f;
+    for (int pr = rlo; pr <= rhi; ++pr) {
+        for (int pc = clo; pc <= chi; ++pc) {
+            TapSet t = warp_taps(w, pr, pc);
+            int dr = qr - t.r0, dc = qc - t.c0;
+            if ((unsigned)dr <= 1u && (unsigned)dc <= 1u) {
+                acc = fmaf(tap_weight(t, dr, dc), __ldg(y + (long long)pr * w.cols + pc), acc);
+            }
+        }
+    }
+    return acc;
+}

@@ -1,0 +1,504 @@
+"""PDHG / SPDHG solvers on sm_100a (mirror of mctomo.solvers, solvers.py:1-498).
+
+Same API surface and semantics as the reference: ``Problem``, ``SolverConfig``
+(admissibility checks), ``default_config`` (strong-convexity-balanced step
+sizes), ``SolverState``, ``SaddlePoint``, ``sample_gates``, ``step``, ``run``,
+``DivergenceError``, ``RHO``.  One iteration is
+
+    (i)   x <- prox_{tau g}(x - tau*zbar)
+    (ii)  for i in S: y_i <- prox_{sigma_i f_i*}(y_i + sigma_i A_i x)
+    (iii) z <- z + sum_i A_i^T dy_i;  zbar <- z + sum_i (theta/p_i) A_i^T dy_i
+
+executed as four fused sm_100a kernels (engine.py).  ``run`` pre-draws the
+SPDHG gate sequence with the *same* numpy generator calls as the reference
+(``default_rng(seed)`` then one ``rng.choice(N, p=p/p.sum())`` per iteration,
+solvers.py:312, :392), uploads it once, and replays one CUDA graph per epoch.
+Solver state lives on the device in fp32; ``SolverState`` exposes it as
+float64 numpy arrays like the reference.
+
+Extensions beyond the reference (the BASELINE workloads need them):
+``run_batch`` (independent slices in one launch per kernel, per-slice seeds)
+and ``distributed.run_pdhg_sharded`` (PDHG gate-sharded over GPUs).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Callable, Sequence
+
+import numpy as np
+
+from . import _lib
+from .engine import Engine
+from .experiment_io import ConvergenceRecord, rmse
+from .functionals import fit_value, g_value, moduli
+from .linops import LinearMap
+
+__all__ = [
+    "RHO",
+    "DivergenceError",
+    "Problem",
+    "SolverConfig",
+    "SolverState",
+    "SaddlePoint",
+    "default_config",
+    "sample_gates",
+    "draw_sequence",
+    "step",
+    "run",
+    "run_batch",
+]
+
+RHO = 0.99  # solvers.py:63
+MODES = ("pdhg", "spdhg")
+
+
+class DivergenceError(RuntimeError):
+    """Raised when a solver run leaves the finite/bounded regime."""
+
+
+@dataclass(frozen=True)
+class Problem:
+    """Saddle point problem data: operators, data blocks, penalty weight."""
+
+    alpha: float
+    operators: tuple
+    data: tuple
+
+    def __post_init__(self):
+        if not self.alpha > 0:
+            raise ValueError("alpha must be positive")
+        if not self.operators:
+            raise ValueError("at least one gate required")
+        if len(self.operators) != len(self.data):
+            raise ValueError("one data block per operator required")
+        dom = tuple(self.operators[0].domain_shape)
+        for k, (op, d) in enumerate(zip(self.operators, self.data)):
+            if tuple(op.domain_shape) != dom:
+                raise ValueError(f"gate {k} domain mismatch")
+            if d.shape != tuple(op.range_shape):
+                raise ValueError(
+                    f"gate {k} data shape {d.shape} != operator range {tuple(op.range_shape)}")
+
+    @classmethod
+    def from_parts(cls, alpha: float, operators: Sequence[LinearMap], data) -> "Problem":
+        return cls(alpha=float(alpha), operators=tuple(operators),
+                   data=tuple(np.asarray(d, dtype=np.float64) for d in data))
+
+    @property
+    def num_gates(self) -> int:
+        return len(self.operators)
+
+    @property
+    def image_shape(self) -> tuple:
+        return tuple(self.operators[0].domain_shape)
+
+    def objective(self, x) -> float:
+        """Full objective; applies every gated operator once (on the device)."""
+        n = self.num_gates
+        total = g_value(self.alpha, x)
+        for op, d in zip(self.operators, self.data):
+            total += fit_value(n, d, op.apply(np.asarray(x, dtype=np.float64)))
+        return total
+
+    def data_objective(self) -> float:
+        n = self.num_gates
+        return sum(fit_value(n, d, np.zeros_like(d)) for d in self.data)
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """Step sizes, sampling law and budget of one run (solvers.py:127-195)."""
+
+    mode: str
+    sigmas: tuple
+    tau: float
+    theta: float
+    probs: tuple
+    epochs: int
+    seed: int
+    gate_norms: tuple
+    stacked_norm_sq: float | None = None
+
+    def __post_init__(self):
+        if self.mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}, got {self.mode!r}")
+        n = len(self.sigmas)
+        if n == 0 or len(self.probs) != n or len(self.gate_norms) != n:
+            raise ValueError("sigmas, probs, gate_norms must share one length >= 1")
+        if not all(s > 0 and math.isfinite(s) for s in self.sigmas):
+            raise ValueError("all sigmas must be positive and finite")
+        if not (self.tau > 0 and math.isfinite(self.tau)):
+            raise ValueError("tau must be positive and finite")
+        if not (0 < self.theta <= 1):
+            raise ValueError("theta must lie in (0, 1]")
+        if not all(0 < p <= 1 for p in self.probs):
+            raise ValueError("probabilities must lie in (0, 1]")
+        if self.mode == "pdhg" and any(p != 1.0 for p in self.probs):
+            raise ValueError("pdhg mode requires all probabilities equal to 1")
+        if self.epochs < 0:
+            raise ValueError("epochs must be >= 0")
+        if not all(v > 0 for v in self.gate_norms):
+            raise ValueError("gate norms must be positive")
+        slack = 1.0 + 1e-9
+        if self.mode == "spdhg":
+            for s, p, v in zip(self.sigmas, self.probs, self.gate_norms):
+                if s * self.tau * v * v > RHO ** 2 * p * slack:
+                    raise ValueError("inadmissible step sizes: sigma*tau*||A_i||^2 exceeds "
+                                     f"RHO^2*p_i for a gate with norm {v:.6g}")
+        else:
+            s2 = (self.stacked_norm_sq if self.stacked_norm_sq is not None
+                  else sum(v * v for v in self.gate_norms))
+            for s in self.sigmas:
+                if s * self.tau * s2 > RHO ** 2 * slack:
+                    raise ValueError("inadmissible step sizes: sigma*tau*||stack||^2 exceeds RHO^2")
+
+    @property
+    def num_gates(self) -> int:
+        return len(self.sigmas)
+
+    @property
+    def iterations_per_epoch(self) -> int:
+        return 1 if self.mode == "pdhg" else self.num_gates
+
+
+def default_config(mode: str, gate_norms: Sequence[float], alpha: float, epochs: int,
+                   seed: int = 0, stacked_norm_sq: float | None = None) -> SolverConfig:
+    """Strong-convexity-balanced step sizes (solvers.py:198-247, the code's rule)."""
+    gate_norms = tuple(float(v) for v in gate_norms)
+    if not gate_norms:
+        raise ValueError("at least one gate norm required")
+    if not all(v > 0 for v in gate_norms):
+        raise ValueError("gate norms must be positive")
+    n = len(gate_norms)
+    mu_g, mu_fstar = moduli(alpha, n)
+    gamma = math.sqrt(mu_g / mu_fstar)
+    if mode == "pdhg":
+        probs = (1.0,) * n
+        s2 = stacked_norm_sq if stacked_norm_sq is not None else sum(v * v for v in gate_norms)
+        s = math.sqrt(s2)
+        sigmas = (gamma * RHO / s,) * n
+        tau = RHO / (gamma * s)
+    elif mode == "spdhg":
+        probs = (1.0 / n,) * n
+        sigmas = tuple(gamma * RHO / v for v in gate_norms)
+        tau = RHO / (gamma * max(v / p for v, p in zip(gate_norms, probs)))
+    else:
+        raise ValueError(f"mode must be one of {MODES}, got {mode!r}")
+    return SolverConfig(mode=mode, sigmas=sigmas, tau=tau, theta=1.0, probs=probs,
+                        epochs=int(epochs), seed=int(seed), gate_norms=gate_norms,
+                        stacked_norm_sq=stacked_norm_sq)
+
+
+@dataclass
+class SaddlePoint:
+    """Primal-dual optimum used as the distance reference (solvers.py:279-295)."""
+
+    x_star: np.ndarray
+    y_star: list
+    source: str
+    converged: bool
+    residual: float
+
+    def distance_sq(self, x, y) -> float:
+        total = float(np.vdot(x - self.x_star, x - self.x_star))
+        for yk, ystar in zip(y, self.y_star):
+            diff = yk - ystar
+            total += float(np.vdot(diff, diff))
+        return total
+
+
+def sample_gates(rng: np.random.Generator, probs: Sequence[float], mode: str) -> tuple:
+    """Draw the gate subset for one iteration (solvers.py:298-313)."""
+    if mode == "pdhg":
+        return tuple(range(len(probs)))
+    if mode == "spdhg":
+        p = np.asarray(probs, dtype=np.float64)
+        return (int(rng.choice(len(probs), p=p / p.sum())),)
+    raise ValueError(f"mode must be one of {MODES}, got {mode!r}")
+
+
+def draw_sequence(config: SolverConfig, iterations: int | None = None,
+                  seed: int | None = None) -> np.ndarray:
+    """The reference's SPDHG gate sequence, drawn up front on the host.
+
+    Makes exactly the generator calls ``run`` makes (solvers.py:392, :395-396),
+    so the sequence is bit-identical to the reference's per-iteration draws.
+    """
+    if config.mode != "spdhg":
+        raise ValueError("only spdhg draws gates at random")
+    if iterations is None:
+        iterations = config.epochs * config.iterations_per_epoch
+    rng = np.random.default_rng(config.seed if seed is None else seed)
+    return np.array([sample_gates(rng, config.probs, "spdhg")[0] for _ in range(iterations)],
+                    dtype=np.int32)
+
+
+# ---------------------------------------------------------------------------
+class SolverState:
+    """Iterate of a run: primal x, duals y_i, aggregates z, zbar, counters.
+
+    Before the first ``step`` the arrays are held on the host; once bound to a
+    problem the device buffers are authoritative and the ``x``, ``y``, ``z``,
+    ``zbar`` attributes read / write float64 numpy copies (solvers.py:250-276).
+    """
+
+    def __init__(self, x, y, z, zbar, iteration: int = 0, epoch: float = 0.0,
+                 fwd_calls: int = 0, adj_calls: int = 0, last_projections=None):
+        self._engine = None
+        self._problem = None
+        self._host = {
+            "x": np.array(x, dtype=np.float64),
+            "y": [np.array(v, dtype=np.float64) for v in y],
+            "z": np.array(z, dtype=np.float64),
+            "zbar": np.array(zbar, dtype=np.float64),
+        }
+        self.iteration = iteration
+        self.epoch = epoch
+        self.fwd_calls = fwd_calls
+        self.adj_calls = adj_calls
+        self._last = dict(last_projections or {})
+
+    @classmethod
+    def zeros(cls, problem: Problem) -> "SolverState":
+        shape = problem.image_shape
+        return cls(x=np.zeros(shape), y=[np.zeros(d.shape) for d in problem.data],
+                   z=np.zeros(shape), zbar=np.zeros(shape))
+
+    # -- device binding ------------------------------------------------------
+    def _bind(self, problem: Problem, keep_projections: bool = True) -> Engine:
+        if self._engine is not None and self._problem is problem:
+            return self._engine
+        torch = _lib.require_cuda()
+        host = self._host if self._engine is None else self._snapshot_host()
+        eng = Engine([problem.operators], [problem.data], keep_projections=keep_projections)
+        eng.x[0].copy_(torch.from_numpy(host["x"].astype(np.float32)))
+        eng.z[0].copy_(torch.from_numpy(host["z"].astype(np.float32)))
+        eng.zbar[0].copy_(torch.from_numpy(host["zbar"].astype(np.float32)))
+        if len(host["y"]) != problem.num_gates:
+            raise ValueError("state has a different number of dual blocks than the problem")
+        for i, v in enumerate(host["y"]):
+            eng.y[0, i].copy_(torch.from_numpy(np.asarray(v, dtype=np.float32)))
+        self._engine, self._problem, self._host = eng, problem, None
+        return eng
+
+    def _snapshot_host(self):
+        return {"x": self.x, "y": self.y, "z": self.z, "zbar": self.zbar}
+
+    def _get(self, name):
+        if self._engine is None:
+            v = self._host[name]
+            return [a for a in v] if name == "y" else v
+        t = getattr(self._engine, name)
+        if name == "y":
+            return [t[0, i].double().cpu().numpy() for i in range(t.shape[1])]
+        return t[0].double().cpu().numpy()
+
+    def _set(self, name, value):
+        if self._engine is None:
+            if name == "y":
+                self._host["y"] = [np.array(v, dtype=np.float64) for v in value]
+            else:
+                self._host[name] = np.array(value, dtype=np.float64)
+            return
+        torch = _lib.require_cuda()
+        t = getattr(self._engine, name)
+        if name == "y":
+            for i, v in enumerate(value):
+                t[0, i].copy_(torch.from_numpy(np.asarray(v, dtype=np.float32)))
+        else:
+            t[0].copy_(torch.from_numpy(np.asarray(value, dtype=np.float32)))
+
+    x = property(lambda s: s._get("x"), lambda s, v: s._set("x", v))
+    y = property(lambda s: s._get("y"), lambda s, v: s._set("y", v))
+    z = property(lambda s: s._get("z"), lambda s, v: s._set("z", v))
+    zbar = property(lambda s: s._get("zbar"), lambda s, v: s._set("zbar", v))
+
+    @property
+    def last_projections(self) -> dict:
+        if self._engine is None or self._engine.proj is None:
+            return dict(self._last)
+        return {i: self._engine.proj[0, i].double().cpu().numpy() for i in self._last}
+
+    @last_projections.setter
+    def last_projections(self, value):
+        self._last = dict(value)
+
+
+def _raise_status(eng: Engine):
+    primal, dual = eng.read_status()
+    if primal is not None and (dual is None or primal <= dual[0]):
+        raise DivergenceError(f"non-finite primal iterate at iteration {primal}")
+    if dual is not None:
+        raise DivergenceError(f"non-finite dual iterate (gate {dual[1]}) at iteration {dual[0]}")
+
+
+def step(state: SolverState, config: SolverConfig, problem: Problem,
+         draw: Callable[[], tuple]) -> SolverState:
+    """Advance the state by one iteration in place (solvers.py:316-366).
+
+    ``draw`` supplies the gate subset; an empty draw is retried.  Raises
+    :class:`DivergenceError` on the first non-finite iterate.
+    """
+    torch = _lib.require_cuda()
+    n = problem.num_gates
+    if config.num_gates != n:
+        raise ValueError("config and problem disagree on the gate count")
+    eng = state._bind(problem)
+    eng.set_params(config)
+    subset = draw()
+    while len(subset) == 0:
+        subset = draw()
+    subset = tuple(int(i) for i in subset)
+    if any(i < 0 or i >= n for i in subset):
+        raise ValueError("drawn gate out of range")
+    if len(set(subset)) != len(subset):
+        raise ValueError("a draw may not repeat a gate within one iteration")
+    gates = torch.tensor(subset, dtype=torch.int32, device=eng.device)
+    eng.iteration(eng.items_subset(gates, len(subset), state.iteration + 1), problem.alpha)
+    _raise_status(eng)
+    state.fwd_calls += len(subset)
+    state.adj_calls += len(subset)
+    state.last_projections = {i: None for i in subset}
+    state.iteration += 1
+    state.epoch += len(subset) / n
+    return state
+
+
+def _guard(problem_data_objective: float) -> float:
+    return 1e6 * max(problem_data_objective, np.finfo(np.float64).tiny)
+
+
+def run(config: SolverConfig, problem: Problem, saddle: SaddlePoint | None = None,
+        truth=None, on_epoch: Callable | None = None, *, graph: bool = True,
+        diagnostics: bool = True):
+    """Run ``config.epochs`` full data passes (solvers.py:369-419).
+
+    Returns ``(x, ConvergenceRecord)`` with x a float64 numpy array.  Per-epoch
+    diagnostics (objective, distance to ``saddle``, rmse to ``truth``) are
+    computed on the device and are not counted as solver work.  With
+    ``diagnostics=False`` the objective column is NaN and only the non-finite
+    iterate checks guard the run (the timed benchmark configuration).
+    """
+    if config.num_gates != problem.num_gates:
+        raise ValueError("config and problem disagree on the gate count")
+    state = SolverState.zeros(problem)
+    record = ConvergenceRecord()
+    if config.epochs == 0:
+        return np.zeros(problem.image_shape), record
+    torch = _lib.require_cuda()
+    keep = diagnostics and config.mode == "pdhg"
+    eng = state._bind(problem, keep_projections=keep)
+    eng.set_params(config)
+    eng.reset()
+    n = problem.num_gates
+    if config.mode == "spdhg":
+        eng.set_sequences(draw_sequence(config)[None, :])
+    guard = _guard(problem.data_objective())
+    ipe = config.iterations_per_epoch
+    g = eng.epoch_graph(config.mode, problem.alpha) if graph else None
+    xs = ys = tr = None
+    if saddle is not None:
+        xs = torch.from_numpy(np.asarray(saddle.x_star, dtype=np.float32)).to(eng.device)
+        ys = torch.from_numpy(np.stack([np.asarray(v, dtype=np.float32)
+                                        for v in saddle.y_star])).to(eng.device)
+    if truth is not None:
+        tr = torch.from_numpy(np.asarray(truth, dtype=np.float32)).to(eng.device)
+    for epoch_index in range(1, config.epochs + 1):
+        if g is not None:
+            g.replay()
+        else:
+            eng.epoch(config.mode, problem.alpha)
+        state.iteration += ipe
+        state.epoch += 1.0
+        state.fwd_calls += n
+        state.adj_calls += n
+        if config.mode == "pdhg":
+            state.last_projections = {i: None for i in range(n)}
+        if diagnostics or on_epoch is not None or epoch_index == config.epochs:
+            _raise_status(eng)
+        objective_value = math.nan
+        if diagnostics:
+            objective_value = eng.objectives(problem.alpha, config.mode == "pdhg")[0]
+            if not math.isfinite(objective_value) or objective_value > guard:
+                raise DivergenceError(
+                    f"objective {objective_value:.3e} exceeded the divergence guard "
+                    f"at epoch {epoch_index} (iteration {state.iteration})")
+        dist = math.nan
+        if xs is not None:
+            dist = float(eng.reduce(eng.x[0], xs, 1, eng.n_img, _lib.REDUCE_SQDIFF).item())
+            dist += float(eng.reduce(eng.y[0], ys, 1, eng.N * eng.n_sino,
+                                     _lib.REDUCE_SQDIFF).item())
+        err = math.nan
+        if tr is not None:
+            err = math.sqrt(float(eng.reduce(eng.x[0], tr, 1, eng.n_img,
+                                             _lib.REDUCE_SQDIFF).item()) / eng.n_img)
+        record.append(epoch=float(epoch_index), dist_sq=dist, objective=objective_value,
+                      rmse_to_truth=err, fwd_calls=state.fwd_calls, adj_calls=state.adj_calls)
+        if on_epoch is not None:
+            on_epoch(epoch_index, state)
+    return state.x, record
+
+
+def run_batch(configs: Sequence[SolverConfig], problems: Sequence[Problem], *,
+              graph: bool = True, diagnostics: bool = False):
+    """Independent slices solved together (BASELINE C5).
+
+    All problems share one geometry, gate count, mode, step-size rule and
+    alpha per slice is honoured only if equal; each slice keeps its own warps,
+    data and sampling seed.  Returns a list of ``(x, ConvergenceRecord)``.
+    """
+    if len(configs) != len(problems) or not problems:
+        raise ValueError("one config per problem required")
+    c0, p0 = configs[0], problems[0]
+    for c, p in zip(configs, problems):
+        if c.num_gates != p.num_gates or p.num_gates != p0.num_gates:
+            raise ValueError("all slices need the same gate count")
+        if (c.mode, c.sigmas, c.tau, c.theta, c.probs, c.epochs) != \
+                (c0.mode, c0.sigmas, c0.tau, c0.theta, c0.probs, c0.epochs):
+            raise ValueError("batched slices must share step sizes and budget (seeds may differ)")
+        if p.alpha != p0.alpha:
+            raise ValueError("batched slices must share alpha")
+    eng = BatchRunner(configs, problems, keep_projections=diagnostics and c0.mode == "pdhg")
+    return eng.run(graph=graph, diagnostics=diagnostics)
+
+
+class BatchRunner:
+    """Engine wrapper for S independent slices (used by run_batch and bench)."""
+
+    def __init__(self, configs, problems, keep_projections=False):
+        self.configs = list(configs)
+        self.problems = list(problems)
+        c0 = self.configs[0]
+        self.engine = Engine([p.operators for p in problems], [p.data for p in problems],
+                             keep_projections=keep_projections)
+        self.engine.set_params(c0)
+        self.mode = c0.mode
+        self.alpha = problems[0].alpha
+        if self.mode == "spdhg":
+            self.engine.set_sequences(np.stack([draw_sequence(c) for c in configs]))
+
+    def run(self, graph=True, diagnostics=False):
+        eng = self.engine
+        c0 = self.configs[0]
+        S = len(self.problems)
+        records = [ConvergenceRecord() for _ in range(S)]
+        eng.reset()
+        g = eng.epoch_graph(self.mode, self.alpha) if graph else None
+        n = c0.num_gates
+        for e in range(1, c0.epochs + 1):
+            if g is not None:
+                g.replay()
+            else:
+                eng.epoch(self.mode, self.alpha)
+            objs = [math.nan] * S
+            if diagnostics:
+                _raise_status(eng)
+                objs = eng.objectives(self.alpha, self.mode == "pdhg")
+            for s in range(S):
+                records[s].append(epoch=float(e), dist_sq=math.nan, objective=objs[s],
+                                  rmse_to_truth=math.nan, fwd_calls=e * n, adj_calls=e * n)
+        _raise_status(eng)
+        xs = eng.x.double().cpu().numpy()
+        return [(xs[s], records[s]) for s in range(S)]

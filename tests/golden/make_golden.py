@@ -1,0 +1,190 @@
+"""Generate golden fixtures from the *imported reference* (run in the build container).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Every array here is an output of the unmodified reference package ``mctomo``
+(/root/reference/pkg/src/mctomo) on seeded inputs; the inputs are fp32-rounded so
+the GPU path and the reference consume identical values.  The reference cannot
+travel to the GPU box, so its outputs are committed as small .npz fixtures.
+Nothing here is copied from the reference tests' data (they hold none on disk).
+"""
+
+from __future__ import annotations
+
+import math
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parent.parent
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, str(ROOT))
+
+from mctomo.linops import power_method, stacked_norm_sq  # noqa: E402
+from mctomo.motion import MotionParams, WarpOperator, motion_sequence  # noqa: E402
+from mctomo.projector import Geometry, ray_transform  # noqa: E402
+from mctomo.simulate import (estimate_norms, gate_operators, gaussian_field,  # noqa: E402
+                             generate, make_phantom)
+from mctomo.solvers import Problem, default_config, run, sample_gates  # noqa: E402
+
+from paper_2410_10503_b200 import workloads  # noqa: E402  (numpy-only input generators)
+
+F32 = lambda a: np.asarray(a, dtype=np.float32).astype(np.float64)  # noqa: E731
+
+PROJECTOR_GEOMS = {
+    "fast": (64, 64, 128, 128, 64.0 * math.sqrt(2.0) / 128.0),
+    "rect_spacing": (33, 21, 24, 40, 1.1),
+    "tiny": (24, 24, 16, 32, math.hypot(24, 24) / 32),
+    "many_angles": (17, 17, 180, 25, 1.0),
+    "axis_exact": (65, 65, 48, 95, 1.0),
+    "half_spacing": (16, 16, 8, 11, 0.5),
+    "lin": (24, 24, 12, 30, 1.2),
+    "c1": (128, 128, 180, 183, 1.0),
+    "odd_rect": (40, 31, 37, 51, 1.0),
+}
+
+WARP_CASES = {
+    "rigid_a": (("rigid", 0.37, (1.3, -0.8), 1.0), (20, 20)),
+    "rigid_b": (("rigid", -0.2, (0.0, 2.7), 1.0), (17, 23)),
+    "dilatation": (("dilatation", 0.0, (0.0, 0.0), 1.06), (20, 20)),
+    "quarter": (("rigid", math.pi / 2.0, (0.0, 0.0), 1.0), (15, 15)),
+    "half": (("rigid", math.pi, (0.0, 0.0), 1.0), (11, 11)),
+    "shift": (("rigid", 0.0, (2.0, 3.0), 1.0), (16, 16)),
+    "out_of_frame": (("rigid", 0.0, (100.0, 0.0), 1.0), (8, 8)),
+    "c1_like": (("rigid", math.radians(4.2), (2.3, -1.7), 1.0), (128, 128)),
+    "shrink": (("dilatation", 0.0, (0.0, 0.0), 0.93), (31, 26)),
+}
+
+
+def projector_cases():
+    rng = np.random.default_rng(20241014)
+    out = {}
+    for name, g in PROJECTOR_GEOMS.items():
+        geom = Geometry(*g)
+        op = ray_transform(geom)
+        x = F32(rng.standard_normal(geom.image_shape))
+        y = F32(rng.standard_normal(geom.sino_shape))
+        out[f"{name}__geom"] = np.array(g, dtype=np.float64)
+        out[f"{name}__x"] = x
+        out[f"{name}__y"] = y
+        out[f"{name}__Ax"] = op.apply(x)
+        out[f"{name}__ATy"] = op.adjoint_apply(y)
+    np.savez_compressed(HERE / "projector.npz", **out)
+
+
+def warp_cases():
+    rng = np.random.default_rng(7)
+    out = {}
+    for name, ((kind, rot, tr, sc), shape) in WARP_CASES.items():
+        op = WarpOperator(MotionParams(kind, rot, tr, sc), shape)
+        x = F32(rng.standard_normal(shape))
+        y = F32(rng.standard_normal(shape))
+        out[f"{name}__params"] = np.array([rot, tr[0], tr[1], sc], dtype=np.float64)
+        out[f"{name}__shape"] = np.array(shape)
+        out[f"{name}__kind"] = np.array(0 if kind == "rigid" else 1)
+        out[f"{name}__x"] = x
+        out[f"{name}__y"] = y
+        out[f"{name}__Dx"] = op.apply(x)
+        out[f"{name}__DTy"] = op.adjoint_apply(y)
+    np.savez_compressed(HERE / "warps.npz", **out)
+
+
+def sampling_cases():
+    out = {}
+    for n in (4, 10, 20):
+        for seed in (0, 5, 42):
+            rng = np.random.default_rng(seed)
+            probs = (1.0 / n,) * n
+            out[f"n{n}_s{seed}"] = np.array(
+                [sample_gates(rng, probs, "spdhg")[0] for _ in range(50 * n)], dtype=np.int32)
+    out["field_5x7_1234_3"] = gaussian_field((5, 7), 1234, 3)
+    out["field_c1_0_2"] = gaussian_field((180, 183), 0, 2)
+    np.savez_compressed(HERE / "sampling.npz", **out)
+
+
+def solver_tiny():
+    geom = Geometry(24, 24, 16, 32, math.hypot(24, 24) / 32)
+    phantom = make_phantom("nested_shells", 24, 24)
+    motion = motion_sequence("rigid", 4, magnitude=0.6)
+    ds = generate(phantom, motion, geom, master_seed=3)
+    data = [F32(s) for s in ds.sinograms]
+    norms = estimate_norms(geom, motion, iterations=40)
+    alpha = norms["base_norm_sq"] / 70.0
+    ops = gate_operators(geom, motion, True)
+    problem = Problem.from_parts(alpha, ops, data)
+    out = {
+        "geom": np.array([24, 24, 16, 32, math.hypot(24, 24) / 32]),
+        "motion": np.array([[m.rotation, m.translation[0], m.translation[1]] for m in motion]),
+        "data": np.stack(data),
+        "truth": phantom,
+        "gate_norms": np.array(norms["gate_norms"]),
+        "stacked_norm_sq": np.array(norms["stacked_norm_sq"]),
+        "base_norm_sq": np.array(norms["base_norm_sq"]),
+        "alpha": np.array(alpha),
+    }
+    for mode, seed in (("pdhg", 0), ("spdhg", 5)):
+        cfg = default_config(mode, norms["gate_norms"], alpha, epochs=10, seed=seed,
+                             stacked_norm_sq=norms["stacked_norm_sq"] if mode == "pdhg" else None)
+        states = {}
+
+        def grab(e, s, states=states):
+            states[e] = (s.x.copy(), [v.copy() for v in s.y], s.z.copy(), s.zbar.copy())
+
+        x, rec = run(cfg, problem, truth=phantom, on_epoch=grab)
+        out[f"{mode}__x"] = x
+        out[f"{mode}__y"] = np.stack(states[10][1])
+        out[f"{mode}__z"] = states[10][2]
+        out[f"{mode}__zbar"] = states[10][3]
+        out[f"{mode}__x_e1"] = states[1][0]
+        out[f"{mode}__objective"] = np.array(rec.objective)
+        out[f"{mode}__rmse"] = np.array(rec.rmse_to_truth)
+        out[f"{mode}__fwd_calls"] = np.array(rec.fwd_calls)
+        out[f"{mode}__sigmas"] = np.array(cfg.sigmas)
+        out[f"{mode}__tau"] = np.array(cfg.tau)
+    np.savez_compressed(HERE / "solver_tiny.npz", **out)
+
+
+def solver_c1():
+    cfg_w = workloads.CONFIGS["c1"]
+    inp = workloads.slice_inputs(cfg_w, 0)
+    geom = Geometry(*cfg_w.geometry_args)
+    motion = [MotionParams("rigid", g["rotation"], tuple(g["translation"])) for g in inp.gates]
+    ops = gate_operators(geom, motion, True)
+    phantom = inp.phantom.astype(np.float64)
+    clean = [op.apply(phantom) for op in ops]
+    data = [F32(d) for d in workloads.noisy_data(clean, inp.seed)]
+    t0 = time.time()
+    norms = estimate_norms(geom, motion, iterations=100)
+    print(f"  c1 norms {time.time() - t0:.1f}s", flush=True)
+    problem = Problem.from_parts(cfg_w.alpha, ops, data)
+    out = {
+        "phantom": inp.phantom,
+        "data": np.stack(data).astype(np.float32),
+        "clean_0": clean[0],
+        "gate_norms": np.array(norms["gate_norms"]),
+        "stacked_norm_sq": np.array(norms["stacked_norm_sq"]),
+        "base_norm_sq": np.array(norms["base_norm_sq"]),
+    }
+    for mode in ("pdhg", "spdhg"):
+        cfg = default_config(mode, norms["gate_norms"], cfg_w.alpha, epochs=cfg_w.epochs,
+                             seed=cfg_w.seed,
+                             stacked_norm_sq=norms["stacked_norm_sq"] if mode == "pdhg" else None)
+        t0 = time.time()
+        x, rec = run(cfg, problem, truth=phantom)
+        print(f"  c1 {mode} {time.time() - t0:.1f}s", flush=True)
+        out[f"{mode}__x"] = x
+        out[f"{mode}__objective"] = np.array(rec.objective)
+        out[f"{mode}__rmse"] = np.array(rec.rmse_to_truth)
+    np.savez_compressed(HERE / "solver_c1.npz", **out)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["projector", "warps", "sampling", "tiny", "c1"]
+    for w in which:
+        t0 = time.time()
+        {"projector": projector_cases, "warps": warp_cases, "sampling": sampling_cases,
+         "tiny": solver_tiny, "c1": solver_c1}[w]()
+        print(f"{w}: {time.time() - t0:.1f}s", flush=True)

@@ -1,0 +1,259 @@
+"""GPU tier: sm_100a operators vs the reference's golden outputs and the oracle.
+
+Bars (BASELINE.json north_star): operator outputs within relative L2 1e-5 of
+the fp64 reference on identical (fp32-rounded) inputs; adjoint identity
+<A x, y> = <x, A^* y> to 1e-5 with fp64 inner products.  Known-answer cases
+follow test_projector.py:62-160 and test_motion.py:47-105 at fp32 tolerances
+(exact where the reference is exact).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5  # north_star operator parity (fp32 vs fp64 reference)
+
+
+@pytest.fixture(scope="module")
+def m():
+    import paper_2410_10503_b200 as m
+
+    m.build_native()
+    return m
+
+
+def _geom(m, g):
+    r, c, a, b, sp = g
+    return m.Geometry(int(r), int(c), int(a), int(b), float(sp))
+
+
+GEOMS = ["fast", "rect_spacing", "tiny", "many_angles", "axis_exact", "half_spacing", "lin",
+         "c1", "odd_rect"]
+
+
+@pytest.mark.parametrize("name", GEOMS)
+def test_ray_forward_adjoint_vs_reference(m, golden_projector, name):
+    G = golden_projector
+    op = m.RayTransform(_geom(m, G[f"{name}__geom"]))
+    ax = op.apply(G[f"{name}__x"])
+    aty = op.adjoint_apply(G[f"{name}__y"])
+    assert ax.dtype == np.float64 and ax.shape == G[f"{name}__Ax"].shape
+    assert rel_l2(ax, G[f"{name}__Ax"]) <= TOL
+    assert rel_l2(aty, G[f"{name}__ATy"]) <= TOL
+
+
+@pytest.mark.parametrize("name", GEOMS)
+def test_ray_adjoint_identity(m, golden_projector, name):
+    op = m.RayTransform(_geom(m, golden_projector[f"{name}__geom"]))
+    assert m.adjoint_mismatch(op, pairs=5, seed=0) <= TOL
+
+
+def test_axis_aligned_one_hot_is_exact(m):
+    geom = m.Geometry(65, 65, 48, 95, 1.0)
+    x = np.zeros((65, 65))
+    x[20, 40] = 1.0
+    sino = m.forward(geom, x)
+    j = (40 - 32) + 47
+    assert sino[0, j] == 1.0
+    row = sino[0].copy()
+    row[j] = 0.0
+    assert np.all(row == 0.0)
+
+
+def test_row_sums_match_tent_sum(m):
+    geom = m.Geometry(65, 65, 48, 95, 1.0)
+    x = np.zeros((65, 65))
+    x[32, 32] = 1.0
+    sino = m.forward(geom, x)
+    centers = geom.bin_centers
+    for a, th in enumerate(geom.angles):
+        mm = max(abs(math.cos(th)), abs(math.sin(th)))
+        expected = np.maximum(0.0, 1.0 - np.abs(centers / mm)).sum() / mm
+        assert sino[a].sum() == pytest.approx(expected, rel=1e-6)
+    assert sino[0].sum() == 1.0
+
+
+def test_center_bin_of_ones_image(m):
+    geom = m.Geometry(64, 64, 36, 95, 64.0 * math.sqrt(2.0) / 95.0)
+    sino = m.forward(geom, np.ones((64, 64)))
+    for a, th in enumerate(geom.angles):
+        mm = max(abs(math.cos(th)), abs(math.sin(th)))
+        assert sino[a, 47] == pytest.approx(64.0 / mm, rel=2e-6)
+
+
+def test_quarter_turn_rotational_consistency(m):
+    geom = m.Geometry(33, 33, 24, 49, 1.0)
+    img = np.random.default_rng(0).random((33, 33))
+    rot = m.WarpOperator(m.MotionParams("rigid", math.pi / 2.0), (33, 33)).apply(img)
+    op = m.ray_transform(geom)
+    s0, s1 = op.apply(img), op.apply(rot)
+    n = geom.num_angles
+    for a in range(n):
+        exp = s0[a - n // 2] if a >= n // 2 else s0[a + n // 2][::-1]
+        assert np.max(np.abs(s1[a] - exp)) <= 1e-5 * np.abs(s0).max()
+
+
+def test_linearity_and_zero(m):
+    geom = m.Geometry(24, 24, 12, 30, 1.2)
+    r = np.random.default_rng(5)
+    a, b = r.random((24, 24)), r.random((24, 24))
+    left = m.forward(geom, 2.0 * a - 3.0 * b)
+    right = 2.0 * m.forward(geom, a) - 3.0 * m.forward(geom, b)
+    assert rel_l2(left, right) <= 1e-6
+    assert np.all(m.forward(geom, np.zeros((24, 24))) == 0.0)
+    with pytest.raises(ValueError):
+        m.forward(geom, np.zeros((24, 23)))
+    with pytest.raises(ValueError):
+        m.adjoint(geom, np.zeros((11, 30)))
+
+
+def test_batched_forward_equals_single(m):
+    import torch
+
+    geom = m.Geometry(48, 40, 30, 70, 1.0)
+    op = m.RayTransform(geom)
+    x = torch.randn(3, 48, 40, device="cuda")
+    yb = op.forward_batch(x)
+    for i in range(3):
+        assert torch.equal(yb[i], op.apply(x[i]))
+    y = torch.randn(3, 30, 70, device="cuda")
+    xb = op.adjoint_batch(y)
+    for i in range(3):
+        assert torch.equal(xb[i], op.adjoint_apply(y[i]))
+
+
+def test_forward_adjoint_deterministic(m):
+    import torch
+
+    op = m.RayTransform(m.Geometry(96, 96, 90, 137, 1.0))
+    x = torch.randn(96, 96, device="cuda")
+    y = torch.randn(90, 137, device="cuda")
+    assert torch.equal(op.apply(x), op.apply(x))
+    assert torch.equal(op.adjoint_apply(y), op.adjoint_apply(y))
+
+
+# ---------------------------------------------------------------- large sizes
+@pytest.mark.parametrize("n,A,B", [(256, 360, 363), (512, 720, 729)])
+def test_ray_parity_vs_oracle_large(m, n, A, B):
+    r = np.random.default_rng(n)
+    x = r.standard_normal((n, n)).astype(np.float32).astype(np.float64)
+    y = r.standard_normal((A, B)).astype(np.float32).astype(np.float64)
+    geom = m.Geometry(n, n, A, B, 1.0)
+    op = m.RayTransform(geom)
+    orc = oracle.RayTransform(oracle.Geometry(n, n, A, B, 1.0), threads=oracle.default_threads())
+    assert rel_l2(op.apply(x), orc.apply(x)) <= TOL
+    assert rel_l2(op.adjoint_apply(y), orc.adjoint_apply(y)) <= TOL
+
+
+@pytest.mark.parametrize("n,A,B", [(512, 720, 729), (1024, 1440, 1453)])
+def test_adjoint_identity_full_size(m, n, A, B):
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    op = m.RayTransform(m.Geometry(n, n, A, B, 1.0))
+    x = torch.randn(n, n, device="cuda", generator=g)
+    y = torch.randn(A, B, device="cuda", generator=g)
+    lhs = float((op.apply(x).double() * y.double()).sum())
+    rhs = float((x.double() * op.adjoint_apply(y).double()).sum())
+    assert abs(lhs - rhs) <= TOL * max(abs(lhs), abs(rhs))
+
+
+# ---------------------------------------------------------------------- warps
+WARPS = ["rigid_a", "rigid_b", "dilatation", "quarter", "half", "shift", "out_of_frame",
+         "c1_like", "shrink"]
+EXACT = {"quarter", "half", "shift", "out_of_frame"}
+
+
+def _warp(m, G, name):
+    rot, tr, tc, sc = G[f"{name}__params"]
+    shape = tuple(int(v) for v in G[f"{name}__shape"])
+    kind = "rigid" if int(G[f"{name}__kind"]) == 0 else "dilatation"
+    if kind == "rigid":
+        p = m.MotionParams("rigid", float(rot), (float(tr), float(tc)))
+    else:
+        p = m.MotionParams("dilatation", scale=float(sc))
+    return m.WarpOperator(p, shape)
+
+
+@pytest.mark.parametrize("name", WARPS)
+def test_warp_vs_reference(m, golden_warps, name):
+    G = golden_warps
+    w = _warp(m, G, name)
+    dx, dty = w.apply(G[f"{name}__x"]), w.adjoint_apply(G[f"{name}__y"])
+    if name in EXACT:
+        assert np.array_equal(dx, G[f"{name}__Dx"])
+        assert np.array_equal(dty, G[f"{name}__DTy"])
+    else:
+        assert rel_l2(dx, G[f"{name}__Dx"]) <= TOL
+        assert rel_l2(dty, G[f"{name}__DTy"]) <= TOL
+    assert m.adjoint_mismatch(w, pairs=5, seed=2) <= TOL
+
+
+def test_identity_warp_copies(m, rng):
+    w = m.WarpOperator(m.MotionParams.identity(), (12, 12))
+    x = rng.random((12, 12))
+    out = w.apply(x)
+    assert np.array_equal(out, x)
+    out[3, 3] = 99.0
+    assert x[3, 3] != 99.0
+
+
+@pytest.mark.parametrize("shape,peak", [((37, 29), 3.0), ((128, 128), 6.0), ((256, 256), 4.0)])
+def test_dense_warp_vs_oracle(m, shape, peak):
+    from paper_2410_10503_b200 import workloads
+
+    r = np.random.default_rng(shape[0])
+    if shape[0] == shape[1]:
+        phi = workloads.bump_field(shape[0], peak, 1, 0)
+    else:
+        phi = (peak * r.standard_normal((2,) + shape)).astype(np.float32)
+    w = m.DenseWarpOperator(phi)
+    o = oracle.Warp(shape, oracle.DENSE, phi=phi)
+    x = r.standard_normal(shape).astype(np.float32).astype(np.float64)
+    y = r.standard_normal(shape).astype(np.float32).astype(np.float64)
+    assert rel_l2(w.apply(x), o.apply(x)) <= TOL
+    assert rel_l2(w.adjoint_apply(y), o.adjoint_apply(y)) <= TOL
+    assert m.adjoint_mismatch(w, pairs=3) <= TOL
+    assert 0 < w.nnz <= 4 * shape[0] * shape[1]
+
+
+def test_gated_operator_is_warp_then_project(m):
+    from paper_2410_10503_b200 import workloads
+
+    geom = m.Geometry(128, 128, 90, 183, 1.0)
+    phi = workloads.bump_field(128, 5.0, 2, 1)
+    dense = m.DenseWarpOperator(phi)
+    rigid = m.WarpOperator(m.MotionParams("rigid", 0.05, (1.2, -0.7)), (128, 128))
+    x = np.random.default_rng(1).random((128, 128))
+    base = m.ray_transform(geom)
+    for w in (dense, rigid):
+        op = m.compose(base, w)
+        assert isinstance(op, m.GatedOperator)
+        assert rel_l2(op.apply(x), base.apply(w.apply(x))) <= 1e-6
+        y = np.random.default_rng(2).standard_normal(geom.sino_shape)
+        assert rel_l2(op.adjoint_apply(y), w.adjoint_apply(base.adjoint_apply(y))) <= 1e-6
+        assert m.adjoint_mismatch(op, pairs=3) <= TOL
+
+
+def test_power_method_matches_reference_norms(m, golden_tiny, golden_c1):
+    from paper_2410_10503_b200 import workloads
+
+    G = golden_tiny
+    r, c, a, b, sp = G["geom"]
+    geom = m.Geometry(int(r), int(c), int(a), int(b), float(sp))
+    motion = [m.MotionParams("rigid", float(p[0]), (float(p[1]), float(p[2]))) for p in G["motion"]]
+    info = m.estimate_norms(geom, motion, iterations=40)
+    assert np.allclose(info["gate_norms"], G["gate_norms"], rtol=1e-4)
+    assert info["stacked_norm_sq"] == pytest.approx(float(G["stacked_norm_sq"]), rel=1e-4)
+    C = golden_c1
+    cfg = workloads.CONFIGS["c1"]
+    inp = workloads.slice_inputs(cfg, 0)
+    info = m.estimate_norms(m.Geometry(*cfg.geometry_args), inp.gates, iterations=100)
+    assert np.allclose(info["gate_norms"], C["gate_norms"], rtol=1e-4)
+    assert info["base_norm_sq"] == pytest.approx(float(C["base_norm_sq"]), rel=1e-4)

@@ -1,0 +1,188 @@
+"""GPU tier: fused PDHG / SPDHG iteration vs the reference's trajectories.
+
+Bar (north_star): iterates after K epochs within relative L2 1e-3 of the fp64
+reference for the same sampling seed and identical step sizes.  Mechanics
+mirror test_solvers.py (counters, determinism, full-sampling equivalence,
+aggregate invariant, divergence guard, empty-draw retry, epochs=0).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import solver as osolver
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+ITER_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def m():
+    import paper_2410_10503_b200 as m
+
+    m.build_native()
+    return m
+
+
+def tiny_problem(m, G):
+    r, c, a, b, sp = G["geom"]
+    geom = m.Geometry(int(r), int(c), int(a), int(b), float(sp))
+    motion = [m.MotionParams("rigid", float(p[0]), (float(p[1]), float(p[2]))) for p in G["motion"]]
+    ops = m.gate_operators(geom, motion, True)
+    return m.Problem.from_parts(float(G["alpha"]), ops, list(G["data"]))
+
+
+def tiny_config(m, G, mode, seed, epochs=10):
+    return m.SolverConfig(mode=mode, sigmas=tuple(G[f"{mode}__sigmas"]),
+                          tau=float(G[f"{mode}__tau"]), theta=1.0,
+                          probs=(1.0,) * 4 if mode == "pdhg" else (0.25,) * 4, epochs=epochs,
+                          seed=seed, gate_norms=tuple(G["gate_norms"]),
+                          stacked_norm_sq=float(G["stacked_norm_sq"]) if mode == "pdhg" else None)
+
+
+@pytest.mark.parametrize("mode,seed", [("pdhg", 0), ("spdhg", 5)])
+@pytest.mark.parametrize("graph", [True, False])
+def test_tiny_trajectory_matches_reference(m, golden_tiny, mode, seed, graph):
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    cfg = tiny_config(m, G, mode, seed)
+    seen = {}
+    x, rec = m.run(cfg, problem, truth=G["truth"], graph=graph,
+                   on_epoch=lambda e, s: seen.setdefault(e, (s.x, s.y, s.z)))
+    assert rel_l2(x, G[f"{mode}__x"]) <= ITER_TOL
+    assert rel_l2(seen[10][2], G[f"{mode}__z"]) <= ITER_TOL
+    assert rel_l2(np.stack(seen[10][1]), G[f"{mode}__y"]) <= ITER_TOL
+    assert rel_l2(seen[1][0], G[f"{mode}__x_e1"]) <= ITER_TOL
+    assert np.allclose(rec.objective, G[f"{mode}__objective"], rtol=ITER_TOL)
+    assert np.allclose(rec.rmse_to_truth, G[f"{mode}__rmse"], rtol=ITER_TOL)
+    assert rec.fwd_calls == list(G[f"{mode}__fwd_calls"])
+    assert rec.adj_calls == rec.fwd_calls
+
+
+@pytest.mark.parametrize("mode", ["pdhg", "spdhg"])
+def test_c1_trajectory_matches_reference(m, golden_c1, mode):
+    from paper_2410_10503_b200 import workloads
+
+    G = golden_c1
+    cfgw = workloads.CONFIGS["c1"]
+    problem, truth, _ = m.simulate.workload_problem(cfgw, 0, data=list(G["data"]))
+    cfg = m.default_config(mode, G["gate_norms"], cfgw.alpha, cfgw.epochs, seed=cfgw.seed,
+                           stacked_norm_sq=float(G["stacked_norm_sq"]) if mode == "pdhg" else None)
+    x, rec = m.run(cfg, problem, truth=truth)
+    assert rel_l2(x, G[f"{mode}__x"]) <= ITER_TOL
+    assert np.allclose(rec.objective, G[f"{mode}__objective"], rtol=ITER_TOL)
+    x2, _ = m.run(cfg, problem, diagnostics=False)
+    assert np.array_equal(x, x2)  # diagnostics do not perturb the iterates
+
+
+def test_dense_spdhg_trajectory_vs_oracle(m):
+    from paper_2410_10503_b200 import workloads
+
+    cfgw = workloads.WorkloadConfig("dense_small", 96, 120, 137, 5, "dense", 6, 1e-2, 3, peak=4.0)
+    problem, truth, inp = m.simulate.workload_problem(cfgw, 0)
+    norms = [m.power_method(op, iterations=30) for op in problem.operators]
+    geom = oracle.Geometry(*cfgw.geometry_args)
+    oops = oracle.gate_operators(geom, inp.gates, threads=oracle.default_threads())
+    for mode in ("spdhg", "pdhg"):
+        cfg = m.default_config(mode, norms, cfgw.alpha, cfgw.epochs, seed=11)
+        x, rec = m.run(cfg, problem)
+        ocfg = osolver.default_config(mode, norms, cfgw.alpha, cfgw.epochs, seed=11)
+        st, objs = osolver.run(ocfg, cfgw.alpha, oops, [np.asarray(d) for d in problem.data])
+        assert rel_l2(x, st.x) <= ITER_TOL, mode
+        assert np.allclose(rec.objective, objs, rtol=ITER_TOL)
+
+
+def test_full_sampling_spdhg_reproduces_pdhg_bitwise(m, golden_tiny):
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    pcfg = tiny_config(m, G, "pdhg", 0, epochs=6)
+    x_pdhg, _ = m.run(pcfg, problem)
+    full = m.SolverConfig(mode="spdhg", sigmas=pcfg.sigmas, tau=pcfg.tau, theta=1.0,
+                          probs=(1.0,) * 4, epochs=6, seed=0, gate_norms=pcfg.gate_norms)
+    st = m.SolverState.zeros(problem)
+    for _ in range(6):
+        m.step(st, full, problem, lambda: (0, 1, 2, 3))
+    assert np.array_equal(st.x, x_pdhg)
+
+
+def test_run_deterministic_and_counters(m, golden_tiny):
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    cfg = tiny_config(m, G, "spdhg", 9, epochs=5)
+    x1, r1 = m.run(cfg, problem)
+    x2, r2 = m.run(cfg, problem)
+    assert np.array_equal(x1, x2) and r1.objective == r2.objective
+    assert r1.fwd_calls == [4, 8, 12, 16, 20]
+
+
+def test_aggregate_invariant_and_single_gate_updates(m, golden_tiny):
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    cfg = tiny_config(m, G, "spdhg", 5)
+    st = m.SolverState.zeros(problem)
+    rng = np.random.default_rng(cfg.seed)
+    for _ in range(25):
+        y_before = st.y
+        m.step(st, cfg, problem, lambda: m.sample_gates(rng, cfg.probs, "spdhg"))
+        recomputed = sum(op.adjoint_apply(y) for op, y in zip(problem.operators, st.y))
+        assert rel_l2(st.z, recomputed) <= 1e-4
+        changed = [i for i, (a, b) in enumerate(zip(st.y, y_before)) if not np.array_equal(a, b)]
+        assert len(changed) <= 1
+    assert st.iteration == 25 and st.fwd_calls == 25 and st.epoch == pytest.approx(25 / 4)
+
+
+def test_empty_draw_is_retried(m, golden_tiny):
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    st = m.SolverState.zeros(problem)
+    draws = iter([(), (), (2,)])
+    m.step(st, tiny_config(m, G, "spdhg", 0), problem, lambda: next(draws))
+    assert st.fwd_calls == 1 and st.iteration == 1
+
+
+def test_epochs_zero_and_gate_mismatch(m, golden_tiny):
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    x, rec = m.run(tiny_config(m, G, "pdhg", 0, epochs=0), problem)
+    assert np.array_equal(x, np.zeros(problem.image_shape)) and len(rec) == 0
+    cfg = m.default_config("spdhg", G["gate_norms"][:3], problem.alpha, 1)
+    with pytest.raises(ValueError, match="gate count"):
+        m.run(cfg, problem)
+
+
+def test_divergence_guard_fires(m, golden_tiny):
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    # norms understated 1000x: wildly inadmissible steps for the true operators
+    cfg = m.default_config("pdhg", np.asarray(G["gate_norms"]) / 1000.0, problem.alpha, 200)
+    with pytest.raises(m.DivergenceError):
+        m.run(cfg, problem)
+
+
+def test_run_batch_equals_single_runs(m):
+    from paper_2410_10503_b200 import workloads
+
+    cfgw = workloads.WorkloadConfig("batch_small", 64, 60, 91, 3, "dense", 5, 1e-2, 4, peak=3.0)
+    probs = [m.simulate.workload_problem(cfgw, s)[0] for s in range(3)]
+    norms = [m.power_method(op, iterations=20) for op in probs[0].operators]
+    cfgs = [m.default_config("spdhg", norms, cfgw.alpha, cfgw.epochs, seed=100 + s)
+            for s in range(3)]
+    out = m.run_batch(cfgs, probs)
+    for (xb, _), c, p in zip(out, cfgs, probs):
+        xs, _ = m.run(c, p, diagnostics=False)
+        assert np.array_equal(xb, xs)
+
+
+def test_dense_state_roundtrip_and_fixed_point(m, golden_tiny):
+    """A state set from numpy arrays is honoured (reference fixed-point tests style)."""
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    st = m.SolverState.zeros(problem)
+    st.x = np.ones(problem.image_shape)
+    assert np.array_equal(st.x, np.ones(problem.image_shape))
+    m.step(st, tiny_config(m, G, "pdhg", 0), problem, lambda: (0, 1, 2, 3))
+    assert st.iteration == 1
