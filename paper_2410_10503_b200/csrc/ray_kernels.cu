@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs p) {
     const int item = blockIdx.z;
     const int a = blockIdx.y * 8 + threadIdx.y;
     const int j = blockIdx.x * 32 + threadIdx.x;
-    if (a >= p.A) return;
+    if (a >= p.A) return;  // warp-uniform (one angle per warp)
     const bool active = j < p.B;
     const RayAngle ra = p.ang[a];
     const char* base = p.ws + (size_t)item * p.item_bytes;
@@ -122,54 +122,62 @@ __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs p) {
     const int nmaj = cd ? p.cols : p.rows;
     const int lim = cd ? p.rows : p.cols;
 
-    float acc = 0.0f;
+    // per-ray range of dominant-axis samples with a tap inside the grid
+    double c0 = 0.0;
+    int lo = nmaj, hi = -1;
     if (active) {
         const double sj = ((double)j - p.jmid) * p.sp;
-        const double c0 = ra.P * sj + ra.Q;
-        int lo, hi;
+        c0 = ra.P * sj + ra.Q;
         if (ra.slope == 0.0) {
             if (c0 > -1.0 && c0 < (double)lim) { lo = 0; hi = nmaj - 1; }
-            else { lo = 0; hi = -1; }
         } else {
-            double ka = (-1.0 - c0) / ra.slope, kb = ((double)lim - c0) / ra.slope;
+            const double ka = (-1.0 - c0) / ra.slope, kb = ((double)lim - c0) / ra.slope;
             const double top = (double)nmaj + 2.0;
-            double kmin = fmin(fmax(fmin(ka, kb), -2.0), top);
-            double kmax = fmin(fmax(fmax(ka, kb), -2.0), top);
+            const double kmin = fmin(fmax(fmin(ka, kb), -2.0), top);
+            const double kmax = fmin(fmax(fmax(ka, kb), -2.0), top);
             lo = max(0, (int)floor(kmin));
             hi = min(nmaj - 1, (int)ceil(kmax));
         }
-        if (lo <= hi) {
-            long long fx = __double2ll_rn((c0 + (double)lo * ra.slope) * 4294967296.0);
-            const long long sfx = ra.slope_fx;
-            const float* row = X + (long long)lo * stride;
-            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-            int k = lo;
-            for (; k + 3 <= hi; k += 4) {
-                const long long f1 = fx + sfx, f2 = f1 + sfx, f3 = f2 + sfx;
-                const float* q0 = row + (int)(fx >> 32);
-                const float* q1 = row + stride + (int)(f1 >> 32);
-                const float* q2 = row + 2 * stride + (int)(f2 >> 32);
-                const float* q3 = row + 3 * stride + (int)(f3 >> 32);
-                float v00 = __ldg(q0), v01 = __ldg(q0 + 1);
-                float v10 = __ldg(q1), v11 = __ldg(q1 + 1);
-                float v20 = __ldg(q2), v21 = __ldg(q2 + 1);
-                float v30 = __ldg(q3), v31 = __ldg(q3 + 1);
-                a0 += fmaf(frac_from_fx((unsigned)fx), v01 - v00, v00);
-                a1 += fmaf(frac_from_fx((unsigned)f1), v11 - v10, v10);
-                a2 += fmaf(frac_from_fx((unsigned)f2), v21 - v20, v20);
-                a3 += fmaf(frac_from_fx((unsigned)f3), v31 - v30, v30);
-                fx = f3 + sfx;
-                row += 4 * stride;
-            }
-            for (; k <= hi; ++k) {
-                const float* q0 = row + (int)(fx >> 32);
-                float v00 = __ldg(q0), v01 = __ldg(q0 + 1);
-                a0 += fmaf(frac_from_fx((unsigned)fx), v01 - v00, v00);
-                fx += sfx;
-                row += stride;
-            }
-            acc = (a0 + a1) + (a2 + a3);
+    }
+    // the warp walks the union of its rays' ranges in lock-step so every load
+    // instruction reads one contiguous segment of one image row (coalesced);
+    // samples whose taps fall outside the grid are predicated off.
+    const int wlo = __reduce_min_sync(0xffffffffu, lo);
+    const int whi = __reduce_max_sync(0xffffffffu, hi);
+    float acc = 0.0f;
+    if (wlo <= whi) {
+        const unsigned lim1 = active ? (unsigned)(lim + 1) : 0u;
+        long long fx = __double2ll_rn((c0 + (double)wlo * ra.slope) * 4294967296.0);
+        const long long sfx = ra.slope_fx;
+        const float* row = X + (long long)wlo * stride;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        int k = wlo;
+#define MCT_FWD_SAMPLE(ACC, FX, ROW)                                           \
+        {                                                                      \
+            const int i0 = (int)((FX) >> 32);                                  \
+            float v0 = 0.f, v1 = 0.f;                                          \
+            if ((unsigned)(i0 + 1) < lim1) {                                   \
+                v0 = __ldg((ROW) + i0);                                        \
+                v1 = __ldg((ROW) + i0 + 1);                                    \
+            }                                                                  \
+            ACC += fmaf(frac_from_fx((unsigned)(FX)), v1 - v0, v0);            \
         }
+        for (; k + 3 <= whi; k += 4) {
+            const long long f1 = fx + sfx, f2 = f1 + sfx, f3 = f2 + sfx;
+            MCT_FWD_SAMPLE(a0, fx, row)
+            MCT_FWD_SAMPLE(a1, f1, row + stride)
+            MCT_FWD_SAMPLE(a2, f2, row + 2 * stride)
+            MCT_FWD_SAMPLE(a3, f3, row + 3 * stride)
+            fx = f3 + sfx;
+            row += 4 * stride;
+        }
+        for (; k <= whi; ++k) {
+            MCT_FWD_SAMPLE(a0, fx, row)
+            fx += sfx;
+            row += stride;
+        }
+#undef MCT_FWD_SAMPLE
+        acc = (a0 + a1) + (a2 + a3);
     }
     const float proj = acc * ra.step;
     if (!active) return;
@@ -201,27 +209,48 @@ __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs p) {
 // (integer bin + fp32 fraction) and offset per pixel in fp32, which keeps the
 // coordinate error ~1e-6 bins at 1024^2.
 // ---------------------------------------------------------------------------
-#define ADJ_TILE 16
-#define ADJ_CH 256
+#define ADJ_TW 32      // tile width (columns) = one warp
+#define ADJ_TH 16      // tile height (rows)
+#define ADJ_PPT 4      // pixels per thread (rows ty, ty+4, ty+8, ty+12)
+#define ADJ_THREADS (ADJ_TW * ADJ_TH / ADJ_PPT)
+#define ADJ_CH ADJ_THREADS
 #define MAGIC_F 12582912.0f  // 1.5 * 2^23
 #define MAGIC_I 0x4B400000
 
+// Each thread owns ADJ_PPT pixels of one tile column so the per-angle constants
+// (two shared-memory broadcasts) are amortised over several pixels; a warp
+// covers 32 consecutive columns of a row, so its bin reads are one contiguous
+// run of the sinogram row (coalesced, L1-resident).
 template <int K>
-__global__ void __launch_bounds__(256) adj_kernel(AdjArgs p, float* out, long long out_stride) {
+__global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(AdjArgs p, float* out,
+                                                          long long out_stride) {
     __shared__ float4 s_a[ADJ_CH];  // f0 - 0.5, cos/sp, sin/sp, step*g
-    __shared__ float4 s_b[ADJ_CH];  // step, step - step*g, row offset (int bits), -
+    __shared__ float2 s_b[ADJ_CH];  // step - step*g/2, row offset (int bits)
+    __shared__ float s_c[ADJ_CH];   // step (general footprint path)
     const int item = blockIdx.z;
-    const int tid = threadIdx.y * ADJ_TILE + threadIdx.x;
-    const int r0 = blockIdx.y * ADJ_TILE, c0 = blockIdx.x * ADJ_TILE;
-    const int r = r0 + threadIdx.y, c = c0 + threadIdx.x;
-    const bool inside = (r < p.rows) && (c < p.cols);
-    const double u0 = (double)r0 + 7.5 - 0.5 * (double)(p.rows - 1);
-    const double v0 = (double)c0 + 7.5 - 0.5 * (double)(p.cols - 1);
-    const float du = (float)threadIdx.y - 7.5f, dv = (float)threadIdx.x - 7.5f;
+    const int tid = threadIdx.y * ADJ_TW + threadIdx.x;
+    const int r0 = blockIdx.y * ADJ_TH, c0 = blockIdx.x * ADJ_TW;
+    const int c = c0 + threadIdx.x;
+    const double u0 = (double)r0 + 0.5 * (ADJ_TH - 1) - 0.5 * (double)(p.rows - 1);
+    const double v0 = (double)c0 + 0.5 * (ADJ_TW - 1) - 0.5 * (double)(p.cols - 1);
+    const float dv = (float)threadIdx.x - 0.5f * (ADJ_TW - 1);
+    float du[ADJ_PPT];
+    bool inside[ADJ_PPT];
+#pragma unroll
+    for (int m = 0; m < ADJ_PPT; ++m) {
+        const int rr = threadIdx.y + (ADJ_TH / ADJ_PPT) * m;
+        inside[m] = (r0 + rr < p.rows) && (c < p.cols);
+        // rows below the image reuse the thread's first row (result discarded) so
+        // every bin read stays inside the padded sinogram
+        du[m] = (float)(inside[m] ? rr : threadIdx.y) - 0.5f * (ADJ_TH - 1);
+    }
     const char* base = p.ws + (size_t)item * p.item_bytes;
     const float* __restrict__ DY = reinterpret_cast<const float*>(base + p.off_dy);
 
-    float acc0 = 0.0f, acc1 = 0.0f;
+    float acc[ADJ_PPT];
+#pragma unroll
+    for (int m = 0; m < ADJ_PPT; ++m) acc[m] = 0.0f;
+    const bool any_inside = inside[0];
     for (int a0 = 0; a0 < p.A; a0 += ADJ_CH) {
         const int cnt = min(ADJ_CH, p.A - a0);
         __syncthreads();
@@ -229,46 +258,55 @@ __global__ void __launch_bounds__(256) adj_kernel(AdjArgs p, float* out, long lo
             const AdjAngle aa = p.ang[a0 + tid];
             const double jc = v0 * aa.cs - u0 * aa.sn + p.jmid;
             const double J = floor(jc);
-            const float f0 = (float)(jc - J);
             const float gs = aa.step * aa.g;
-            s_a[tid] = make_float4(f0 - 0.5f, (float)aa.cs, (float)aa.sn, gs);
-            s_b[tid] = make_float4(aa.step, aa.step - gs,
-                                   __int_as_float((a0 + tid) * p.wy + p.pb + (int)J), 0.0f);
+            s_a[tid] = make_float4((float)(jc - J) - 0.5f, (float)aa.cs, (float)aa.sn, gs);
+            s_b[tid] = make_float2(aa.step - 0.5f * gs,
+                                   __int_as_float((a0 + tid) * p.wy + p.pb + (int)J));
+            s_c[tid] = aa.step;
         }
         __syncthreads();
-        if (inside) {
+        if (!any_inside) continue;
 #pragma unroll 2
-            for (int t = 0; t < cnt; ++t) {
-                const float4 A4 = s_a[t];
-                const float4 B4 = s_b[t];
-                const float tm = fmaf(dv, A4.y, fmaf(-du, A4.z, A4.x));  // jc - J - 0.5
-                const float tb = tm + MAGIC_F;
-                const int kf = __float_as_int(tb) - MAGIC_I;              // ~floor(jc - J)
-                const float d = (tm - (tb - MAGIC_F)) + 0.5f;            // jc - J - kf
-                const float* q = DY + (__float_as_int(B4.z) + kf);
-                if (K == 0) {
-                    const float w0 = fmaxf(0.0f, fmaf(-d, A4.w, B4.x));
-                    const float w1 = fmaxf(0.0f, fmaf(d, A4.w, B4.y));
-                    acc0 = fmaf(w0, __ldg(q), acc0);
-                    acc1 = fmaf(w1, __ldg(q + 1), acc1);
-                } else {
+        for (int t = 0; t < cnt; ++t) {
+            const float4 A4 = s_a[t];
+            const float2 B2 = s_b[t];
+            const float tv = fmaf(dv, A4.y, A4.x);  // anchor fraction - 0.5 + dv*cos/sp
+            const float* q = DY + __float_as_int(B2.y);
 #pragma unroll
-                    for (int m = -K; m <= K + 1; ++m) {
-                        const float dist = fabsf((float)m - d);
-                        const float w = fmaxf(0.0f, fmaf(-dist, A4.w, B4.x));
-                        acc0 = fmaf(w, __ldg(q + m), acc0);
+            for (int m = 0; m < ADJ_PPT; ++m) {
+                const float tm = fmaf(-du[m], A4.z, tv);        // jc - J - 0.5
+                const float tb = tm + MAGIC_F;
+                const int kf = __float_as_int(tb) - MAGIC_I;     // ~floor(jc - J)
+                const float e = tm - (tb - MAGIC_F);             // jc - J - kf - 0.5
+                const float* qq = q + kf;
+                if (K == 0) {
+                    // bins kf, kf+1 at distances 0.5+e, 0.5-e
+                    const float w0 = fmaxf(0.0f, fmaf(-e, A4.w, B2.x));
+                    const float w1 = fmaxf(0.0f, fmaf(e, A4.w, B2.x));
+                    acc[m] = fmaf(w0, __ldg(qq), acc[m]);
+                    acc[m] = fmaf(w1, __ldg(qq + 1), acc[m]);
+                } else {
+                    const float step = s_c[t];
+                    const float d = e + 0.5f;
+#pragma unroll
+                    for (int mm = -K; mm <= K + 1; ++mm) {
+                        const float dist = fabsf((float)mm - d);
+                        const float w = fmaxf(0.0f, fmaf(-dist, A4.w, step));
+                        acc[m] = fmaf(w, __ldg(qq + mm), acc[m]);
                     }
                 }
             }
         }
     }
-    if (inside) {
-        const float v = acc0 + acc1;
+#pragma unroll
+    for (int m = 0; m < ADJ_PPT; ++m) {
+        if (!inside[m]) continue;
+        const int r = r0 + threadIdx.y + (ADJ_TH / ADJ_PPT) * m;
         if (out) {
-            out[(long long)item * out_stride + (long long)r * p.cols + c] = v;
+            out[(long long)item * out_stride + (long long)r * p.cols + c] = acc[m];
         } else {
             float* IMG = reinterpret_cast<float*>(const_cast<char*>(base) + p.off_img);
-            IMG[(long long)r * p.cols + c] = v;
+            IMG[(long long)r * p.cols + c] = acc[m];
         }
     }
 }
@@ -299,8 +337,8 @@ cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st) {
 
 cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, float* out,
                        long long out_item_stride, cudaStream_t st) {
-    dim3 block(ADJ_TILE, ADJ_TILE),
-        grid((a.cols + ADJ_TILE - 1) / ADJ_TILE, (a.rows + ADJ_TILE - 1) / ADJ_TILE, items);
+    dim3 block(ADJ_TW, ADJ_TH / ADJ_PPT),
+        grid((a.cols + ADJ_TW - 1) / ADJ_TW, (a.rows + ADJ_TH - 1) / ADJ_TH, items);
     switch (kfoot) {
         case 0: adj_kernel<0><<<grid, block, 0, st>>>(a, out, out_item_stride); break;
         case 1: adj_kernel<1><<<grid, block, 0, st>>>(a, out, out_item_stride); break;
