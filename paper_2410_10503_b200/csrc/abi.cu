@@ -107,6 +107,8 @@ AdjArgs adj_args(const mct_ray_plan* rp, const void* ws) {
     a.item_bytes = rp->item_bytes;
     a.off_dy = rp->off_dy;
     a.off_img = rp->off_img;
+    a.img_slot_bytes = rp->img_slot_bytes;
+    a.asplit = 1;
     return a;
 }
 
@@ -134,6 +136,8 @@ UpdArgs upd_args(const mct_ray_plan* rp, const void* ws) {
     a.ws = static_cast<const char*>(ws);
     a.item_bytes = rp->item_bytes;
     a.off_img = rp->off_img;
+    a.img_slot_bytes = rp->img_slot_bytes;
+    a.asplit = 1;
     return a;
 }
 }  // namespace
@@ -209,6 +213,8 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
         r.slope_fx = llrint(r.slope * 4294967296.0);
         adj[a].cs = c / spacing;
         adj[a].sn = s / spacing;
+        adj[a].csx = llrint(c / spacing * 4294967296.0);
+        adj[a].snx = llrint(s / spacing * 4294967296.0);
         adj[a].step = (float)(1.0 / m);
         adj[a].g = (float)(spacing / m);
         hmax = std::max(hmax, m / spacing);
@@ -233,7 +239,8 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     p->off_dy = off;
     off += align256((size_t)num_angles * p->wy * sizeof(float));
     p->off_img = off;
-    off += align256((size_t)rows * cols * sizeof(float));
+    p->img_slot_bytes = align256((size_t)rows * cols * sizeof(float));
+    off += p->img_slot_bytes * MCT_MAX_ASPLIT;
     p->item_bytes = off;
 
     cudaError_t e = cudaMalloc(&p->d_fwd, sizeof(RayAngle) * num_angles);
@@ -291,8 +298,13 @@ int mct_ray_adjoint(const mct_ray_plan* rp, const float* sino, float* img, int b
                              rp->wy, rp->pb, batch, st),
              "pad sinogram");
     AdjArgs aa = adj_args(rp, ws);
-    MCT_CUDA(launch_adj(aa, rp->kfoot, batch, img, (long long)rp->rows * rp->cols, st),
-             "ray adjoint");
+    aa.asplit = choose_asplit(rp, batch);
+    MCT_CUDA(launch_adj(aa, rp->kfoot, batch, st), "ray adjoint");
+    UpdArgs ua = upd_args(rp, ws);
+    ua.asplit = aa.asplit;
+    ua.sel = single_sel(batch);
+    ua.out = img;
+    MCT_CUDA(launch_update(ua, 0, batch, st), "ray adjoint (partials)");
     return MCT_OK;
 }
 
@@ -441,6 +453,7 @@ int mct_warp_adjoint(const mct_warp_plan* plan, const float* y, float* out, void
     a.rows = plan->desc.rows;
     a.cols = plan->desc.cols;
     a.img_override = y;
+    a.asplit = 1;
     a.sel = single_sel(1);
     a.warps = plan->d_desc;
     a.out = out;
@@ -549,8 +562,10 @@ int mct_gated_adjoint(const mct_family* fam, int slice, int gate, const float* y
                              rp->wy, rp->pb, 1, st),
              "pad sinogram");
     AdjArgs aa = adj_args(rp, ws);
-    MCT_CUDA(launch_adj(aa, rp->kfoot, 1, nullptr, 0, st), "gated adjoint (A^*)");
+    aa.asplit = choose_asplit(rp, 1);
+    MCT_CUDA(launch_adj(aa, rp->kfoot, 1, st), "gated adjoint (A^*)");
     UpdArgs ua = upd_args(rp, ws);
+    ua.asplit = aa.asplit;
     ua.sel = single_sel(1);
     ua.warps = fam->d_warps + (size_t)slice * fam->N + gate;
     ua.out = img;
@@ -605,9 +620,9 @@ int mct_iter_adjoint(const mct_family* fam, const mct_items* it, void* ws, void*
     if (rc) return rc;
     MCT_REQUIRE(ws, "null workspace");
     AdjArgs aa = adj_args(fam->ray, ws);
-    MCT_CUDA(launch_adj(aa, fam->ray->kfoot, it->items_per_slice * it->num_slices, nullptr, 0,
-                        (cudaStream_t)stream),
-             "adjoint");
+    const int items = it->items_per_slice * it->num_slices;
+    aa.asplit = choose_asplit(fam->ray, items);
+    MCT_CUDA(launch_adj(aa, fam->ray->kfoot, items, (cudaStream_t)stream), "adjoint");
     return MCT_OK;
 }
 
@@ -618,6 +633,7 @@ int mct_iter_adjoint_update(const mct_family* fam, const mct_items* it, mct_stat
     MCT_REQUIRE(fam->params_set, "mct_family_set_params has not been called");
     MCT_REQUIRE(s && s->x && s->x_next && ws, "null state buffer");
     UpdArgs ua = upd_args(fam->ray, ws);
+    ua.asplit = choose_asplit(fam->ray, it->items_per_slice * it->num_slices);
     ua.sel = make_sel(it);
     ua.N = fam->N;
     ua.warps = fam->d_warps;

@@ -31,9 +31,15 @@ struct RayAngle {
 // centre (u, v) is jc = (v*cos - u*sin)/sp + (B-1)/2 and the Joseph weight of
 // bin j is step * max(0, 1 - |j - jc| * g) with g = sp*step (tent footprint).
 struct AdjAngle {
-    double cs, sn;  // cos/sp, sin/sp
+    double cs, sn;            // cos/sp, sin/sp
+    long long csx, snx;       // cos/sp, sin/sp in 32.32 fixed point
     float step, g;
 };
+
+// A^* splits its angle loop over up to MCT_MAX_ASPLIT blocks per tile when one
+// launch has too few tiles to fill 148 SMs (single-gate SPDHG); each split
+// writes its own partial image slot and K4 sums the slots in a fixed order.
+#define MCT_MAX_ASPLIT 8
 
 struct mct_ray_plan {
     int rows, cols, A, B;
@@ -44,7 +50,7 @@ struct mct_ray_plan {
     int has_rows, has_cols;
     RayAngle* d_fwd;
     AdjAngle* d_adj;
-    size_t off_x, off_xt, off_dy, off_img, item_bytes;
+    size_t off_x, off_xt, off_dy, off_img, img_slot_bytes, item_bytes;
 };
 
 // --------------------------------------------------------------- warp plan --
@@ -145,13 +151,15 @@ struct AdjArgs {
     int A, B, rows, cols, wy, pb;
     double jmid;
     const char* ws;
-    size_t item_bytes, off_dy, off_img;
+    size_t item_bytes, off_dy, off_img, img_slot_bytes;
+    int asplit;
 };
 
 struct UpdArgs {
     int rows, cols;
     const char* ws;
-    size_t item_bytes, off_img;
+    size_t item_bytes, off_img, img_slot_bytes;
+    int asplit;
     const float* img_override;  // plain D^* of a caller image (single item)
     ItemSel sel;
     int N;
@@ -170,8 +178,8 @@ cudaError_t launch_pack(const PackArgs& a, int items, cudaStream_t st);
 cudaError_t launch_pad_sino(const float* sino, char* ws, size_t item_bytes, size_t off_dy, int A,
                             int B, int wy, int pb, int items, cudaStream_t st);
 cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st);
-cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, float* out,
-                       long long out_item_stride, cudaStream_t st);
+cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, cudaStream_t st);
+int choose_asplit(const mct_ray_plan* rp, int items);
 cudaError_t launch_update(const UpdArgs& a, int mode, int slices, cudaStream_t st);
 cudaError_t launch_z_update(long long n, const float* dz, float* z, float* zbar, float theta,
                             cudaStream_t st);

@@ -150,8 +150,7 @@ __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs p) {
         long long fx = __double2ll_rn((c0 + (double)wlo * ra.slope) * 4294967296.0);
         const long long sfx = ra.slope_fx;
         const float* row = X + (long long)wlo * stride;
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-        int k = wlo;
+        double dacc = 0.0;
 #define MCT_FWD_SAMPLE(ACC, FX, ROW)                                           \
         {                                                                      \
             const int i0 = (int)((FX) >> 32);                                  \
@@ -162,22 +161,30 @@ __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs p) {
             }                                                                  \
             ACC += fmaf(frac_from_fx((unsigned)(FX)), v1 - v0, v0);            \
         }
-        for (; k + 3 <= whi; k += 4) {
-            const long long f1 = fx + sfx, f2 = f1 + sfx, f3 = f2 + sfx;
-            MCT_FWD_SAMPLE(a0, fx, row)
-            MCT_FWD_SAMPLE(a1, f1, row + stride)
-            MCT_FWD_SAMPLE(a2, f2, row + 2 * stride)
-            MCT_FWD_SAMPLE(a3, f3, row + 3 * stride)
-            fx = f3 + sfx;
-            row += 4 * stride;
-        }
-        for (; k <= whi; ++k) {
-            MCT_FWD_SAMPLE(a0, fx, row)
-            fx += sfx;
-            row += stride;
+        // fp32 partial sums over chunks of <= 64 samples, chunk totals in fp64:
+        // the accumulation error stays ~1e-7 relative at n = 1024
+        for (int kc = wlo; kc <= whi; kc += 64) {
+            const int kend = min(whi, kc + 63);
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+            int k = kc;
+            for (; k + 3 <= kend; k += 4) {
+                const long long f1 = fx + sfx, f2 = f1 + sfx, f3 = f2 + sfx;
+                MCT_FWD_SAMPLE(a0, fx, row)
+                MCT_FWD_SAMPLE(a1, f1, row + stride)
+                MCT_FWD_SAMPLE(a2, f2, row + 2 * stride)
+                MCT_FWD_SAMPLE(a3, f3, row + 3 * stride)
+                fx = f3 + sfx;
+                row += 4 * stride;
+            }
+            for (; k <= kend; ++k) {
+                MCT_FWD_SAMPLE(a0, fx, row)
+                fx += sfx;
+                row += stride;
+            }
+            dacc += (double)((a0 + a1) + (a2 + a3));
         }
 #undef MCT_FWD_SAMPLE
-        acc = (a0 + a1) + (a2 + a3);
+        acc = (float)dacc;
     }
     const float proj = acc * ra.step;
     if (!active) return;
@@ -210,105 +217,104 @@ __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs p) {
 // coordinate error ~1e-6 bins at 1024^2.
 // ---------------------------------------------------------------------------
 #define ADJ_TW 32      // tile width (columns) = one warp
-#define ADJ_TH 16      // tile height (rows)
-#define ADJ_PPT 4      // pixels per thread (rows ty, ty+4, ty+8, ty+12)
+#define ADJ_TH 32      // tile height (rows)
+#define ADJ_PPT 8      // consecutive rows per thread
 #define ADJ_THREADS (ADJ_TW * ADJ_TH / ADJ_PPT)
 #define ADJ_CH ADJ_THREADS
-#define MAGIC_F 12582912.0f  // 1.5 * 2^23
-#define MAGIC_I 0x4B400000
 
-// Each thread owns ADJ_PPT pixels of one tile column so the per-angle constants
-// (two shared-memory broadcasts) are amortised over several pixels; a warp
-// covers 32 consecutive columns of a row, so its bin reads are one contiguous
-// run of the sinogram row (coalesced, L1-resident).
+// K3: A^* as a deterministic transpose-gather (no atomics).  Pixel (r, c) at
+// angle a receives  step * max(0, 1 - |j - jc|*g) * dy[a, j]  from the bins j
+// around its detector coordinate jc = (v cos - u sin)/sp + (B-1)/2: exactly the
+// Joseph weight of projector.py:161-166 seen from the pixel (the tent identity
+// pinned by test_projector.py:78-93).
+// jc is carried in 32.32 fixed point: an fp64 anchor per (tile, angle) plus
+// exact integer steps cos/sp, sin/sp per column / row, so the bin index and the
+// interpolation fraction are exact to ~1e-9 bins at any image size.
+// Each thread owns 8 consecutive rows of one column: the two shared-memory
+// broadcasts of the per-angle constants are amortised over 8 pixels, and a warp
+// reads one contiguous run of a sinogram row per pixel row (coalesced, L1).
+// The angle loop may be split over blockIdx.z (partial image slots, summed in a
+// fixed order by K4).  fp32 partial sums per chunk of 128 angles, fp64 totals.
 template <int K>
-__global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(AdjArgs p, float* out,
-                                                          long long out_stride) {
-    __shared__ float4 s_a[ADJ_CH];  // f0 - 0.5, cos/sp, sin/sp, step*g
-    __shared__ float2 s_b[ADJ_CH];  // step - step*g/2, row offset (int bits)
-    __shared__ float s_c[ADJ_CH];   // step (general footprint path)
-    const int item = blockIdx.z;
+__global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(AdjArgs p) {
+    __shared__ longlong2 s_t[ADJ_CH];  // anchor (with sinogram row base), cos/sp
+    __shared__ int4 s_u[ADJ_CH];       // sin/sp (lo, hi), step, step*g
+    const int item = blockIdx.z / p.asplit;
+    const int split = blockIdx.z - item * p.asplit;
+    const int a_beg = (int)((long long)p.A * split / p.asplit);
+    const int a_end = (int)((long long)p.A * (split + 1) / p.asplit);
     const int tid = threadIdx.y * ADJ_TW + threadIdx.x;
     const int r0 = blockIdx.y * ADJ_TH, c0 = blockIdx.x * ADJ_TW;
     const int c = c0 + threadIdx.x;
-    const double u0 = (double)r0 + 0.5 * (ADJ_TH - 1) - 0.5 * (double)(p.rows - 1);
-    const double v0 = (double)c0 + 0.5 * (ADJ_TW - 1) - 0.5 * (double)(p.cols - 1);
-    const float dv = (float)threadIdx.x - 0.5f * (ADJ_TW - 1);
-    float du[ADJ_PPT];
-    bool inside[ADJ_PPT];
-#pragma unroll
-    for (int m = 0; m < ADJ_PPT; ++m) {
-        const int rr = threadIdx.y + (ADJ_TH / ADJ_PPT) * m;
-        inside[m] = (r0 + rr < p.rows) && (c < p.cols);
-        // rows below the image reuse the thread's first row (result discarded) so
-        // every bin read stays inside the padded sinogram
-        du[m] = (float)(inside[m] ? rr : threadIdx.y) - 0.5f * (ADJ_TH - 1);
-    }
+    const int rt = r0 + threadIdx.y * ADJ_PPT;
+    const int nrows = min(ADJ_PPT, p.rows - rt);         // warp-uniform
+    const int txc = min((int)threadIdx.x, p.cols - 1 - c0);  // clamp lanes past the image
+    const double u0 = (double)r0 - 0.5 * (double)(p.rows - 1);
+    const double v0 = (double)c0 - 0.5 * (double)(p.cols - 1);
     const char* base = p.ws + (size_t)item * p.item_bytes;
     const float* __restrict__ DY = reinterpret_cast<const float*>(base + p.off_dy);
+    const long long row_off = (long long)(threadIdx.y * ADJ_PPT);
 
-    float acc[ADJ_PPT];
+    double tot[ADJ_PPT];
 #pragma unroll
-    for (int m = 0; m < ADJ_PPT; ++m) acc[m] = 0.0f;
-    const bool any_inside = inside[0];
-    for (int a0 = 0; a0 < p.A; a0 += ADJ_CH) {
-        const int cnt = min(ADJ_CH, p.A - a0);
+    for (int m = 0; m < ADJ_PPT; ++m) tot[m] = 0.0;
+    for (int a0 = a_beg; a0 < a_end; a0 += ADJ_CH) {
+        const int cnt = min(ADJ_CH, a_end - a0);
         __syncthreads();
         if (tid < cnt) {
             const AdjAngle aa = p.ang[a0 + tid];
-            const double jc = v0 * aa.cs - u0 * aa.sn + p.jmid;
-            const double J = floor(jc);
-            const float gs = aa.step * aa.g;
-            s_a[tid] = make_float4((float)(jc - J) - 0.5f, (float)aa.cs, (float)aa.sn, gs);
-            s_b[tid] = make_float2(aa.step - 0.5f * gs,
-                                   __int_as_float((a0 + tid) * p.wy + p.pb + (int)J));
-            s_c[tid] = aa.step;
+            const double jcA = v0 * aa.cs - u0 * aa.sn + p.jmid;
+            const long long TA = __double2ll_rn(jcA * 4294967296.0) +
+                                 ((long long)((a0 + tid) * p.wy + p.pb) << 32);
+            s_t[tid] = make_longlong2(TA, aa.csx);
+            s_u[tid] = make_int4((int)(unsigned)aa.snx, (int)(aa.snx >> 32),
+                                 __float_as_int(aa.step), __float_as_int(aa.step * aa.g));
         }
         __syncthreads();
-        if (!any_inside) continue;
+        if (nrows <= 0) continue;
+        float acc[ADJ_PPT];
+#pragma unroll
+        for (int m = 0; m < ADJ_PPT; ++m) acc[m] = 0.0f;
 #pragma unroll 2
         for (int t = 0; t < cnt; ++t) {
-            const float4 A4 = s_a[t];
-            const float2 B2 = s_b[t];
-            const float tv = fmaf(dv, A4.y, A4.x);  // anchor fraction - 0.5 + dv*cos/sp
-            const float* q = DY + __float_as_int(B2.y);
+            const longlong2 T2 = s_t[t];
+            const int4 U = s_u[t];
+            const long long snx = ((long long)U.y << 32) | (unsigned)U.x;
+            const float step = __int_as_float(U.z), gs = __int_as_float(U.w);
+            const float h = step - gs;
+            long long T = T2.x + (long long)txc * T2.y - row_off * snx;
 #pragma unroll
             for (int m = 0; m < ADJ_PPT; ++m) {
-                const float tm = fmaf(-du[m], A4.z, tv);        // jc - J - 0.5
-                const float tb = tm + MAGIC_F;
-                const int kf = __float_as_int(tb) - MAGIC_I;     // ~floor(jc - J)
-                const float e = tm - (tb - MAGIC_F);             // jc - J - kf - 0.5
-                const float* qq = q + kf;
-                if (K == 0) {
-                    // bins kf, kf+1 at distances 0.5+e, 0.5-e
-                    const float w0 = fmaxf(0.0f, fmaf(-e, A4.w, B2.x));
-                    const float w1 = fmaxf(0.0f, fmaf(e, A4.w, B2.x));
-                    acc[m] = fmaf(w0, __ldg(qq), acc[m]);
-                    acc[m] = fmaf(w1, __ldg(qq + 1), acc[m]);
-                } else {
-                    const float step = s_c[t];
-                    const float d = e + 0.5f;
+                if (m < nrows) {
+                    const int kf = (int)(T >> 32);                // bin index (incl. row base)
+                    const float d = frac_from_fx((unsigned)T);     // jc - floor(jc) in [0,1)
+                    const float* qq = DY + kf;
+                    if (K == 0) {
+                        const float w0 = fmaxf(0.0f, fmaf(-d, gs, step));  // bin floor(jc)
+                        const float w1 = fmaxf(0.0f, fmaf(d, gs, h));      // bin floor(jc)+1
+                        acc[m] = fmaf(w0, __ldg(qq), acc[m]);
+                        acc[m] = fmaf(w1, __ldg(qq + 1), acc[m]);
+                    } else {
 #pragma unroll
-                    for (int mm = -K; mm <= K + 1; ++mm) {
-                        const float dist = fabsf((float)mm - d);
-                        const float w = fmaxf(0.0f, fmaf(-dist, A4.w, step));
-                        acc[m] = fmaf(w, __ldg(qq + mm), acc[m]);
+                        for (int mm = -K; mm <= K + 1; ++mm) {
+                            const float dist = fabsf((float)mm - d);
+                            const float w = fmaxf(0.0f, fmaf(-dist, gs, step));
+                            acc[m] = fmaf(w, __ldg(qq + mm), acc[m]);
+                        }
                     }
                 }
+                T -= snx;
             }
         }
-    }
 #pragma unroll
-    for (int m = 0; m < ADJ_PPT; ++m) {
-        if (!inside[m]) continue;
-        const int r = r0 + threadIdx.y + (ADJ_TH / ADJ_PPT) * m;
-        if (out) {
-            out[(long long)item * out_stride + (long long)r * p.cols + c] = acc[m];
-        } else {
-            float* IMG = reinterpret_cast<float*>(const_cast<char*>(base) + p.off_img);
-            IMG[(long long)r * p.cols + c] = acc[m];
-        }
+        for (int m = 0; m < ADJ_PPT; ++m) tot[m] += (double)acc[m];
     }
+    if (c >= p.cols) return;
+    float* IMG = reinterpret_cast<float*>(const_cast<char*>(base) + p.off_img +
+                                          (size_t)split * p.img_slot_bytes);
+#pragma unroll
+    for (int m = 0; m < ADJ_PPT; ++m)
+        if (m < nrows) IMG[(long long)(rt + m) * p.cols + c] = (float)tot[m];
 }
 
 }  // namespace
@@ -335,15 +341,25 @@ cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, float* out,
-                       long long out_item_stride, cudaStream_t st) {
+int choose_asplit(const mct_ray_plan* rp, int items) {
+    const long long tiles = (long long)((rp->cols + ADJ_TW - 1) / ADJ_TW) *
+                            ((rp->rows + ADJ_TH - 1) / ADJ_TH) * (items > 0 ? items : 1);
+    const long long target = 148LL * 8;  // >= 8 resident blocks per SM
+    long long s = (target + tiles - 1) / tiles;
+    s = s < 1 ? 1 : s;
+    s = s > MCT_MAX_ASPLIT ? MCT_MAX_ASPLIT : s;
+    const long long by_angles = rp->A / 16 > 0 ? rp->A / 16 : 1;  // >= 16 angles per split
+    return (int)(s < by_angles ? s : by_angles);
+}
+
+cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, cudaStream_t st) {
     dim3 block(ADJ_TW, ADJ_TH / ADJ_PPT),
-        grid((a.cols + ADJ_TW - 1) / ADJ_TW, (a.rows + ADJ_TH - 1) / ADJ_TH, items);
+        grid((a.cols + ADJ_TW - 1) / ADJ_TW, (a.rows + ADJ_TH - 1) / ADJ_TH, items * a.asplit);
     switch (kfoot) {
-        case 0: adj_kernel<0><<<grid, block, 0, st>>>(a, out, out_item_stride); break;
-        case 1: adj_kernel<1><<<grid, block, 0, st>>>(a, out, out_item_stride); break;
-        case 2: adj_kernel<2><<<grid, block, 0, st>>>(a, out, out_item_stride); break;
-        case 3: adj_kernel<3><<<grid, block, 0, st>>>(a, out, out_item_stride); break;
+        case 0: adj_kernel<0><<<grid, block, 0, st>>>(a); break;
+        case 1: adj_kernel<1><<<grid, block, 0, st>>>(a); break;
+        case 2: adj_kernel<2><<<grid, block, 0, st>>>(a); break;
+        case 3: adj_kernel<3><<<grid, block, 0, st>>>(a); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -27,16 +27,24 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs p) {
         const int item = slice * p.sel.ips + k;
         int s_, gate, iter;
         resolve_item(p.sel, item, s_, gate, iter);
-        const float* img = p.img_override
-                               ? p.img_override
-                               : reinterpret_cast<const float*>(p.ws + (size_t)item * p.item_bytes +
-                                                                p.off_img);
+        const char* img = p.img_override
+                              ? reinterpret_cast<const char*>(p.img_override)
+                              : p.ws + (size_t)item * p.item_bytes + p.off_img;
+        const int asplit = p.asplit;
+        const size_t slot = p.img_slot_bytes;
+        // sum of the adjoint's partial-image slots, fixed order
+        auto fetch = [&](long long e) -> float {
+            float v = __ldg(reinterpret_cast<const float*>(img) + e);
+            for (int s = 1; s < asplit; ++s)
+                v += __ldg(reinterpret_cast<const float*>(img + s * slot) + e);
+            return v;
+        };
         float v;
         if (p.warps == nullptr) {
-            v = __ldg(img + q);
+            v = fetch(q);
         } else {
             const WarpDesc& wd = p.warps[p.sel.gates ? (long long)slice * p.N + gate : 0];
-            v = warp_adjoint_at(wd, img, qr, qc);
+            v = warp_adjoint_at(wd, fetch, qr, qc);
         }
         sum += v;
         if (MODE == 1) wsum = fmaf(p.gp[gate].theta_over_p, v, wsum);

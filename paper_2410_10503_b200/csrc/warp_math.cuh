@@ -88,15 +88,16 @@ __device__ __forceinline__ float warp_apply_at(const WarpDesc& w, int r, int c, 
 }
 
 // Transpose at pixel q = (qr, qc): sum over output pixels p with q among taps(p)
-// of w(p, q) * y[p].  Deterministic gather (fixed candidate order).
-__device__ __forceinline__ float warp_adjoint_at(const WarpDesc& w, const float* __restrict__ y,
-                                                 int qr, int qc) {
-    if (w.kind == MCT_WARP_IDENTITY) return __ldg(y + (long long)qr * w.cols + qc);
+// of w(p, q) * y[p], reading y through `fetch(flat_index)`.  Deterministic
+// gather (fixed candidate order).
+template <typename Fetch>
+__device__ __forceinline__ float warp_adjoint_at(const WarpDesc& w, Fetch fetch, int qr, int qc) {
+    if (w.kind == MCT_WARP_IDENTITY) return fetch((long long)qr * w.cols + qc);
     if (w.kind == MCT_WARP_DENSE) {
         const long long q = (long long)qr * w.cols + qc;
         int e0 = __ldg(w.tptr + q), e1 = __ldg(w.tptr + q + 1);
         float acc = 0.0f;
-        for (int e = e0; e < e1; ++e) acc = fmaf(__ldg(w.tw + e), __ldg(y + __ldg(w.tidx + e)), acc);
+        for (int e = e0; e < e1; ++e) acc = fmaf(__ldg(w.tw + e), fetch(__ldg(w.tidx + e)), acc);
         return acc;
     }
     // affine: candidates p in the bounding box of T([q-1, q+1]^2)
@@ -113,7 +114,7 @@ __device__ __forceinline__ float warp_adjoint_at(const WarpDesc& w, const float*
             TapSet t = warp_taps(w, pr, pc);
             int dr = qr - t.r0, dc = qc - t.c0;
             if ((unsigned)dr <= 1u && (unsigned)dc <= 1u) {
-                acc = fmaf(tap_weight(t, dr, dc), __ldg(y + (long long)pr * w.cols + pc), acc);
+                acc = fmaf(tap_weight(t, dr, dc), fetch((long long)pr * w.cols + pc), acc);
             }
         }
     }
