@@ -232,12 +232,14 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     p->pb = pb;
     p->wy = num_bins + 2 * pb;
     size_t off = 0;
+    // pair-packed layouts: element i holds (v[i], v[i+1]) so one 8-byte load
+    // fetches both interpolation taps
     p->off_x = off;
-    off += align256((size_t)rows * p->wx * sizeof(float));
+    off += align256((size_t)rows * p->wx * sizeof(float2));
     p->off_xt = off;
-    off += align256((size_t)cols * p->wxt * sizeof(float));
+    off += align256((size_t)cols * p->wxt * sizeof(float2));
     p->off_dy = off;
-    off += align256((size_t)num_angles * p->wy * sizeof(float));
+    off += align256((size_t)num_angles * p->wy * sizeof(float2));
     p->off_img = off;
     p->img_slot_bytes = align256((size_t)rows * cols * sizeof(float));
     off += p->img_slot_bytes * MCT_MAX_ASPLIT;

@@ -2,11 +2,13 @@
 //
 // Data layout in HBM:
 //   image x            : (rows, cols) fp32 row-major
-//   padded image X     : (rows, wx)  wx = cols + 2*PADX, column c at offset PADX + c
-//   padded transpose XT: (cols, wxt) wxt = rows + 2*PADX, row r of x at offset PADX + r
-//   padded sinogram DY : (A, wy)     wy = B + 2*pb,      bin j at offset pb + j
+//   padded image X2    : (rows, wx) float2, wx = cols + 2*PADX; element PADX + c of
+//                        row r holds (x[r][c], x[r][c+1])  (pair-packed taps)
+//   padded transpose XT2: (cols, wxt) float2, wxt = rows + 2*PADX, the same for x^T
+//   padded sinogram DY2: (A, wy) float2, wy = B + 2*pb, element pb + j holds
+//                        (dy[a][j], dy[a][j+1])
 // Pad regions are zero-initialised once (workspace contract) and never written,
-// so the Joseph gather loops run branch-free.
+// so the Joseph gather loops need no bounds checks.
 #pragma once
 
 #include <cuda_runtime.h>

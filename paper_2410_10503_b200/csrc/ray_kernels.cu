@@ -1,5 +1,5 @@
-// sm_100a kernels of the hot path: fused prox+warp+pack, Joseph forward with
-// fused dual prox, pixel-driven transpose-gather adjoint.
+// sm_100a kernels of the hot path: fused prox+warp+pack (K1), Joseph forward with
+// fused dual prox (K2), pixel-driven transpose-gather adjoint (K3).
 //
 // Reference: projector.py:126-217 (Joseph traversal tables, gather/scatter),
 // motion.py:132-183 (warp), functionals.py:40-68 (proxes), solvers.py:316-366.
@@ -12,8 +12,9 @@ namespace {
 
 // ---------------------------------------------------------------------------
 // K1 / pack: W = D_g(x_new), x_new = prox_g(x - tau*zbar) (or x_new = x), written
-// into the padded row-major X and padded transposed XT of the item workspace.
-// Tile 32x32, block 32x8, transposed store staged through shared memory.
+// into the pair-packed padded row-major X2 and transposed XT2 of the item
+// workspace.  Tile 32x32, block 32x8, the transposed store staged through smem.
+// Pair packing: value W[r][c] is stored as X2[r][c].x and X2[r][c-1].y.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) pack_kernel(PackArgs p) {
     __shared__ float tile[32][33];
@@ -42,8 +43,8 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs p) {
     };
 
     char* base = p.ws + (size_t)item * p.item_bytes;
-    float* X = reinterpret_cast<float*>(base + p.off_x);
-    float* XT = reinterpret_cast<float*>(base + p.off_xt);
+    float* X = reinterpret_cast<float*>(base + p.off_x) + 2 * MCT_PADX;
+    float* XT = reinterpret_cast<float*>(base + p.off_xt) + 2 * MCT_PADX;
 
     const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -59,7 +60,9 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs p) {
             } else {
                 w = warp_apply_at(wd, r, c, xnew);
             }
-            X[(long long)r * p.wx + MCT_PADX + c] = w;
+            const long long e = 2 * ((long long)r * p.wx + c);
+            X[e] = w;
+            X[e - 1] = w;
             if (writer) {
                 float xn = xnew(r, c);
                 p.x_next[(long long)slice * p.x_slice_stride + (long long)r * cols + c] = xn;
@@ -75,35 +78,55 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs p) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         int c = c0 + ty + 8 * k, r = r0 + tx;
-        if (r < rows && c < cols) XT[(long long)c * p.wxt + MCT_PADX + r] = tile[tx][ty + 8 * k];
+        if (r < rows && c < cols) {
+            const long long e = 2 * ((long long)c * p.wxt + r);
+            const float w = tile[tx][ty + 8 * k];
+            XT[e] = w;
+            XT[e - 1] = w;
+        }
     }
 }
 
-// Copy a plain (A, B) sinogram into the padded DY layout of each item.
+// Copy a plain (A, B) sinogram into the pair-packed padded DY2 of each item.
 __global__ void pad_sino_kernel(const float* __restrict__ sino, char* ws, size_t item_bytes,
                                 size_t off_dy, int A, int B, int wy, int pb) {
     const int item = blockIdx.z;
     const int a = blockIdx.y;
     float* DY = reinterpret_cast<float*>(ws + (size_t)item * item_bytes + off_dy);
     const float* s = sino + ((long long)item * A + a) * B;
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x)
-        DY[(long long)a * wy + pb + j] = s[j];
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x) {
+        const long long e = 2 * ((long long)a * wy + pb + j);
+        const float v = s[j];
+        DY[e] = v;
+        DY[e - 1] = v;
+    }
 }
 
 // ---------------------------------------------------------------------------
 // K2: Joseph forward A (projector.py:201-207 with the weights of :160-183).
 // Block = 8 warps = 8 consecutive angles x 32 consecutive bins: the warps walk
-// nearly the same image lines so most of the 2 taps per sample hit L1.
+// nearly the same image lines, so the taps stay L1-resident.
 // Along the dominant axis the continuous minor index advances by a constant
-// slope; it is carried in 32.32 fixed point (integer part = tap index, fraction
-// = interpolation weight), anchored on a per-ray fp64 start, so no float
-// conversions sit in the inner loop.  Rows that cannot contribute are skipped
-// analytically; the padded layout keeps the loop branch-free.
+// slope.  It is carried in 32.32 fixed point whose integer part also carries
+// the row offset, so one 64-bit add advances both, the integer part is the
+// pair-packed tap address and the low word is the interpolation fraction; the
+// start is anchored per ray in fp64.  Each warp walks the union of its 32 rays'
+// sample ranges in lock-step (every load = one contiguous row segment); the
+// common core of the ranges runs without predicates, the ragged edges with.
+// fp32 partial sums per 64-sample chunk, fp64 chunk totals.
 // MODE 0: plain store.  MODE 1: fused dual prox (functionals.py:53-68,
-// solvers.py:341-357) writing y, dy (padded, for K3) and optionally proj.
+// solvers.py:341-357) writing y, dy (pair-packed, for K3) and optionally proj.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float frac_from_fx(unsigned lo) {
-    return __uint_as_float(0x3f800000u | (lo >> 9)) - 1.0f;
+#define FX_ONE 4294967296.0
+#define INV_2_24 5.9604644775390625e-08f
+
+// 32.32 fixed-point add / subtract on an explicit (lo, hi) register pair, so the
+// integer part stays a plain 32-bit register usable as an unsigned index.
+__device__ __forceinline__ void fx_add(unsigned& lo, unsigned& hi, unsigned ilo, unsigned ihi) {
+    asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(lo), "+r"(hi) : "r"(ilo), "r"(ihi));
+}
+__device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo, unsigned ihi) {
+    asm("sub.cc.u32 %0, %0, %2;\n\tsubc.u32 %1, %1, %3;" : "+r"(lo), "+r"(hi) : "r"(ilo), "r"(ihi));
 }
 
 template <int MODE>
@@ -113,78 +136,108 @@ __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs p) {
     const int j = blockIdx.x * 32 + threadIdx.x;
     if (a >= p.A) return;  // warp-uniform (one angle per warp)
     const bool active = j < p.B;
+    const int jj = active ? j : p.B - 1;  // idle lanes shadow the last bin (no store)
     const RayAngle ra = p.ang[a];
     const char* base = p.ws + (size_t)item * p.item_bytes;
     const int cd = ra.cols_dom;
-    const float* __restrict__ X =
-        reinterpret_cast<const float*>(base + (cd ? p.off_xt : p.off_x)) + MCT_PADX;
+    // tap index = hi(fx) >= 0: the row pad is folded into fx so the address is one
+    // unsigned 32x64 multiply-add
+    const float2* __restrict__ X2 =
+        reinterpret_cast<const float2*>(base + (cd ? p.off_xt : p.off_x));
     const int stride = cd ? p.wxt : p.wx;
     const int nmaj = cd ? p.cols : p.rows;
     const int lim = cd ? p.rows : p.cols;
 
-    // per-ray range of dominant-axis samples with a tap inside the grid
-    double c0 = 0.0;
+    // per-ray range of dominant-axis samples that can have a tap inside the grid
+    const double sj = ((double)jj - p.jmid) * p.sp;
+    const double c0 = ra.P * sj + ra.Q;
     int lo = nmaj, hi = -1;
-    if (active) {
-        const double sj = ((double)j - p.jmid) * p.sp;
-        c0 = ra.P * sj + ra.Q;
-        if (ra.slope == 0.0) {
-            if (c0 > -1.0 && c0 < (double)lim) { lo = 0; hi = nmaj - 1; }
-        } else {
-            const double ka = (-1.0 - c0) / ra.slope, kb = ((double)lim - c0) / ra.slope;
-            const double top = (double)nmaj + 2.0;
-            const double kmin = fmin(fmax(fmin(ka, kb), -2.0), top);
-            const double kmax = fmin(fmax(fmax(ka, kb), -2.0), top);
-            lo = max(0, (int)floor(kmin));
-            hi = min(nmaj - 1, (int)ceil(kmax));
-        }
+    if (ra.slope == 0.0) {
+        if (c0 > -1.0 && c0 < (double)lim) { lo = 0; hi = nmaj - 1; }
+    } else {
+        const double ka = (-1.0 - c0) / ra.slope, kb = ((double)lim - c0) / ra.slope;
+        const double top = (double)nmaj + 2.0;
+        const double kmin = fmin(fmax(fmin(ka, kb), -2.0), top);
+        const double kmax = fmin(fmax(fmax(ka, kb), -2.0), top);
+        lo = max(0, (int)floor(kmin));
+        hi = min(nmaj - 1, (int)ceil(kmax));
     }
-    // the warp walks the union of its rays' ranges in lock-step so every load
-    // instruction reads one contiguous segment of one image row (coalesced);
-    // samples whose taps fall outside the grid are predicated off.
-    const int wlo = __reduce_min_sync(0xffffffffu, lo);
+    const int wlo = __reduce_min_sync(0xffffffffu, lo);  // union of the warp's ranges
     const int whi = __reduce_max_sync(0xffffffffu, hi);
+    int clo = __reduce_max_sync(0xffffffffu, lo);        // common core
+    int chi = __reduce_min_sync(0xffffffffu, hi);
     float acc = 0.0f;
     if (wlo <= whi) {
-        const unsigned lim1 = active ? (unsigned)(lim + 1) : 0u;
-        long long fx = __double2ll_rn((c0 + (double)wlo * ra.slope) * 4294967296.0);
-        const long long sfx = ra.slope_fx;
-        const float* row = X + (long long)wlo * stride;
+        if (clo > chi) { clo = whi + 1; chi = whi; }     // no common core: all edge
+        const long long inc64 = ra.slope_fx + ((long long)stride << 32);
+        const unsigned ilo = (unsigned)inc64, ihi = (unsigned)(inc64 >> 32);
+        const long long fx0 = __double2ll_rn((c0 + (double)wlo * ra.slope) * FX_ONE) +
+                              ((long long)(wlo * stride + MCT_PADX) << 32);
+        unsigned flo = (unsigned)fx0, fhi = (unsigned)(fx0 >> 32);
+        int rowoff = wlo * stride + MCT_PADX;
+        const unsigned lim1 = (unsigned)(lim + 1);
         double dacc = 0.0;
-#define MCT_FWD_SAMPLE(ACC, FX, ROW)                                           \
-        {                                                                      \
-            const int i0 = (int)((FX) >> 32);                                  \
-            float v0 = 0.f, v1 = 0.f;                                          \
-            if ((unsigned)(i0 + 1) < lim1) {                                   \
-                v0 = __ldg((ROW) + i0);                                        \
-                v1 = __ldg((ROW) + i0 + 1);                                    \
-            }                                                                  \
-            ACC += fmaf(frac_from_fx((unsigned)(FX)), v1 - v0, v0);            \
-        }
-        // fp32 partial sums over chunks of <= 64 samples, chunk totals in fp64:
-        // the accumulation error stays ~1e-7 relative at n = 1024
-        for (int kc = wlo; kc <= whi; kc += 64) {
-            const int kend = min(whi, kc + 63);
-            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-            int k = kc;
-            for (; k + 3 <= kend; k += 4) {
-                const long long f1 = fx + sfx, f2 = f1 + sfx, f3 = f2 + sfx;
-                MCT_FWD_SAMPLE(a0, fx, row)
-                MCT_FWD_SAMPLE(a1, f1, row + stride)
-                MCT_FWD_SAMPLE(a2, f2, row + 2 * stride)
-                MCT_FWD_SAMPLE(a3, f3, row + 3 * stride)
-                fx = f3 + sfx;
-                row += 4 * stride;
+        float ea = 0.0f;  // ragged-edge samples (predicated on the tap range)
+        int k = wlo;
+        for (; k < clo; ++k) {
+            const int i0 = (int)fhi - rowoff;
+            if ((unsigned)(i0 + 1) < lim1) {
+                const float2 v = __ldg(X2 + fhi);
+                ea += fmaf((float)(flo >> 8) * INV_2_24, v.y - v.x, v.x);
             }
-            for (; k <= kend; ++k) {
-                MCT_FWD_SAMPLE(a0, fx, row)
-                fx += sfx;
-                row += stride;
-            }
-            dacc += (double)((a0 + a1) + (a2 + a3));
+            fx_add(flo, fhi, ilo, ihi);
+            rowoff += stride;
         }
-#undef MCT_FWD_SAMPLE
-        acc = (float)dacc;
+        // core: every lane's taps are inside the padded row (pads read zero)
+        for (int kc = k; kc <= chi; kc += 64) {
+            const int kend = min(chi, kc + 63);
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // sum of v0
+            float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;  // sum of frac*2^24*(v1 - v0)
+            int kk = kc;
+            for (; kk + 3 <= kend; kk += 4) {
+                unsigned l1 = flo, h1 = fhi;
+                fx_add(l1, h1, ilo, ihi);
+                unsigned l2 = l1, h2 = h1;
+                fx_add(l2, h2, ilo, ihi);
+                unsigned l3 = l2, h3 = h2;
+                fx_add(l3, h3, ilo, ihi);
+                const float2 v0 = __ldg(X2 + fhi);
+                const float2 v1 = __ldg(X2 + h1);
+                const float2 v2 = __ldg(X2 + h2);
+                const float2 v3 = __ldg(X2 + h3);
+                s0 += v0.x;
+                s1 += v1.x;
+                s2 += v2.x;
+                s3 += v3.x;
+                t0 = fmaf((float)(flo >> 8), v0.y - v0.x, t0);
+                t1 = fmaf((float)(l1 >> 8), v1.y - v1.x, t1);
+                t2 = fmaf((float)(l2 >> 8), v2.y - v2.x, t2);
+                t3 = fmaf((float)(l3 >> 8), v3.y - v3.x, t3);
+                flo = l3;
+                fhi = h3;
+                fx_add(flo, fhi, ilo, ihi);
+            }
+            for (; kk <= kend; ++kk) {
+                const float2 v0 = __ldg(X2 + fhi);
+                s0 += v0.x;
+                t0 = fmaf((float)(flo >> 8), v0.y - v0.x, t0);
+                fx_add(flo, fhi, ilo, ihi);
+            }
+            dacc += (double)((s0 + s1) + (s2 + s3)) +
+                    (double)((t0 + t1) + (t2 + t3)) * (double)INV_2_24;
+            k = kend + 1;
+        }
+        rowoff = k * stride + MCT_PADX;
+        for (; k <= whi; ++k) {
+            const int i0 = (int)fhi - rowoff;
+            if ((unsigned)(i0 + 1) < lim1) {
+                const float2 v = __ldg(X2 + fhi);
+                ea += fmaf((float)(flo >> 8) * INV_2_24, v.y - v.x, v.x);
+            }
+            fx_add(flo, fhi, ilo, ihi);
+            rowoff += stride;
+        }
+        acc = (float)(dacc + (double)ea);
     }
     const float proj = acc * ra.step;
     if (!active) return;
@@ -200,7 +253,10 @@ __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs p) {
         const float yn = (fmaf(gp.sigma, proj, yv) - gp.sigma * dv) * gp.dual_inv;
         p.y[off] = yn;
         float* DY = reinterpret_cast<float*>(const_cast<char*>(base) + p.off_dy);
-        DY[(long long)a * p.wy + p.pb + j] = yn - yv;
+        const long long e = 2 * ((long long)a * p.wy + p.pb + j);
+        const float dlt = yn - yv;
+        DY[e] = dlt;
+        DY[e - 1] = dlt;
         if (p.proj) p.proj[off] = proj;
         if (!isfinite(yn) && p.status)
             atomicMin(p.status + 1, ((unsigned long long)iter << 20) | (unsigned long long)gate);
@@ -208,20 +264,6 @@ __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs p) {
 }
 
 // ---------------------------------------------------------------------------
-// K3: A^* as a deterministic transpose-gather (no atomics).  Pixel (r, c) at
-// angle a receives  step * max(0, 1 - |j - jc|*g) * dy[a, j]  from the bins j
-// around its detector coordinate jc — exactly the Joseph weight of
-// projector.py:161-166 seen from the pixel (the tent identity pinned by
-// test_projector.py:78-93).  jc is anchored per 16x16 tile and angle in fp64
-// (integer bin + fp32 fraction) and offset per pixel in fp32, which keeps the
-// coordinate error ~1e-6 bins at 1024^2.
-// ---------------------------------------------------------------------------
-#define ADJ_TW 32      // tile width (columns) = one warp
-#define ADJ_TH 32      // tile height (rows)
-#define ADJ_PPT 8      // consecutive rows per thread
-#define ADJ_THREADS (ADJ_TW * ADJ_TH / ADJ_PPT)
-#define ADJ_CH ADJ_THREADS
-
 // K3: A^* as a deterministic transpose-gather (no atomics).  Pixel (r, c) at
 // angle a receives  step * max(0, 1 - |j - jc|*g) * dy[a, j]  from the bins j
 // around its detector coordinate jc = (v cos - u sin)/sp + (B-1)/2: exactly the
@@ -232,13 +274,53 @@ __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs p) {
 // interpolation fraction are exact to ~1e-9 bins at any image size.
 // Each thread owns 8 consecutive rows of one column: the two shared-memory
 // broadcasts of the per-angle constants are amortised over 8 pixels, and a warp
-// reads one contiguous run of a sinogram row per pixel row (coalesced, L1).
+// reads one contiguous run of a sinogram row per pixel row (coalesced, L1); the
+// two bins of a pixel come from one pair-packed 8-byte load.
 // The angle loop may be split over blockIdx.z (partial image slots, summed in a
 // fixed order by K4).  fp32 partial sums per chunk of 128 angles, fp64 totals.
+// ---------------------------------------------------------------------------
+#define ADJ_TW 32      // tile width (columns) = one warp
+#define ADJ_TH 32      // tile height (rows)
+#define ADJ_PPT 8      // consecutive rows per thread
+#define ADJ_THREADS (ADJ_TW * ADJ_TH / ADJ_PPT)
+#define ADJ_CH ADJ_THREADS
+#define INV_2_32 2.3283064365386963e-10f
+
+template <int K, bool FULL>
+__device__ __forceinline__ void adj_angle(const float2* __restrict__ DY2, unsigned tlo,
+                                          unsigned thi, unsigned slo, unsigned shi, float step,
+                                          float gs32, float h, int nrows,
+                                          float (&acc)[ADJ_PPT]) {
+#pragma unroll
+    for (int m = 0; m < ADJ_PPT; ++m) {
+        if (FULL || m < nrows) {
+            // thi = sinogram row base + floor(jc) (>= 0), tlo = frac(jc) * 2^32
+            const float F = (float)tlo;
+            if (K == 0) {
+                const float2 v = __ldg(DY2 + thi);
+                const float w0 = fmaxf(0.0f, fmaf(-F, gs32, step));  // bin floor(jc)
+                const float w1 = fmaxf(0.0f, fmaf(F, gs32, h));      // bin floor(jc) + 1
+                acc[m] = fmaf(w0, v.x, fmaf(w1, v.y, acc[m]));
+            } else {
+                const float d = F * INV_2_32;
+                const float gs = gs32 * 4294967296.0f;
+#pragma unroll
+                for (int mm = -K; mm <= K; mm += 2) {
+                    const float2 v = __ldg(DY2 + (int)thi + mm);
+                    const float wa = fmaxf(0.0f, fmaf(-fabsf((float)mm - d), gs, step));
+                    const float wb = fmaxf(0.0f, fmaf(-fabsf((float)(mm + 1) - d), gs, step));
+                    acc[m] = fmaf(wa, v.x, fmaf(wb, v.y, acc[m]));
+                }
+            }
+        }
+        fx_sub(tlo, thi, slo, shi);
+    }
+}
+
 template <int K>
 __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(AdjArgs p) {
     __shared__ longlong2 s_t[ADJ_CH];  // anchor (with sinogram row base), cos/sp
-    __shared__ int4 s_u[ADJ_CH];       // sin/sp (lo, hi), step, step*g
+    __shared__ int4 s_u[ADJ_CH];       // sin/sp (lo, hi), step, step*g*2^-32
     const int item = blockIdx.z / p.asplit;
     const int split = blockIdx.z - item * p.asplit;
     const int a_beg = (int)((long long)p.A * split / p.asplit);
@@ -247,12 +329,12 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(AdjArgs p) {
     const int r0 = blockIdx.y * ADJ_TH, c0 = blockIdx.x * ADJ_TW;
     const int c = c0 + threadIdx.x;
     const int rt = r0 + threadIdx.y * ADJ_PPT;
-    const int nrows = min(ADJ_PPT, p.rows - rt);         // warp-uniform
-    const int txc = min((int)threadIdx.x, p.cols - 1 - c0);  // clamp lanes past the image
+    const int nrows = min(ADJ_PPT, p.rows - rt);              // warp-uniform
+    const int txc = min((int)threadIdx.x, p.cols - 1 - c0);   // clamp lanes past the image
     const double u0 = (double)r0 - 0.5 * (double)(p.rows - 1);
     const double v0 = (double)c0 - 0.5 * (double)(p.cols - 1);
     const char* base = p.ws + (size_t)item * p.item_bytes;
-    const float* __restrict__ DY = reinterpret_cast<const float*>(base + p.off_dy);
+    const float2* __restrict__ DY2 = reinterpret_cast<const float2*>(base + p.off_dy);
     const long long row_off = (long long)(threadIdx.y * ADJ_PPT);
 
     double tot[ADJ_PPT];
@@ -264,46 +346,39 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(AdjArgs p) {
         if (tid < cnt) {
             const AdjAngle aa = p.ang[a0 + tid];
             const double jcA = v0 * aa.cs - u0 * aa.sn + p.jmid;
-            const long long TA = __double2ll_rn(jcA * 4294967296.0) +
+            const long long TA = __double2ll_rn(jcA * FX_ONE) +
                                  ((long long)((a0 + tid) * p.wy + p.pb) << 32);
             s_t[tid] = make_longlong2(TA, aa.csx);
             s_u[tid] = make_int4((int)(unsigned)aa.snx, (int)(aa.snx >> 32),
-                                 __float_as_int(aa.step), __float_as_int(aa.step * aa.g));
+                                 __float_as_int(aa.step), __float_as_int(aa.step * aa.g * INV_2_32));
         }
         __syncthreads();
         if (nrows <= 0) continue;
         float acc[ADJ_PPT];
 #pragma unroll
         for (int m = 0; m < ADJ_PPT; ++m) acc[m] = 0.0f;
+        if (nrows == ADJ_PPT) {
 #pragma unroll 2
-        for (int t = 0; t < cnt; ++t) {
-            const longlong2 T2 = s_t[t];
-            const int4 U = s_u[t];
-            const long long snx = ((long long)U.y << 32) | (unsigned)U.x;
-            const float step = __int_as_float(U.z), gs = __int_as_float(U.w);
-            const float h = step - gs;
-            long long T = T2.x + (long long)txc * T2.y - row_off * snx;
-#pragma unroll
-            for (int m = 0; m < ADJ_PPT; ++m) {
-                if (m < nrows) {
-                    const int kf = (int)(T >> 32);                // bin index (incl. row base)
-                    const float d = frac_from_fx((unsigned)T);     // jc - floor(jc) in [0,1)
-                    const float* qq = DY + kf;
-                    if (K == 0) {
-                        const float w0 = fmaxf(0.0f, fmaf(-d, gs, step));  // bin floor(jc)
-                        const float w1 = fmaxf(0.0f, fmaf(d, gs, h));      // bin floor(jc)+1
-                        acc[m] = fmaf(w0, __ldg(qq), acc[m]);
-                        acc[m] = fmaf(w1, __ldg(qq + 1), acc[m]);
-                    } else {
-#pragma unroll
-                        for (int mm = -K; mm <= K + 1; ++mm) {
-                            const float dist = fabsf((float)mm - d);
-                            const float w = fmaxf(0.0f, fmaf(-dist, gs, step));
-                            acc[m] = fmaf(w, __ldg(qq + mm), acc[m]);
-                        }
-                    }
-                }
-                T -= snx;
+            for (int t = 0; t < cnt; ++t) {
+                const longlong2 T2 = s_t[t];
+                const int4 U = s_u[t];
+                const long long snx = ((long long)U.y << 32) | (unsigned)U.x;
+                const float step = __int_as_float(U.z), gs32 = __int_as_float(U.w);
+                const float h = fmaf(-4294967296.0f, gs32, step);
+                const long long T = T2.x + (long long)txc * T2.y - row_off * snx;
+                adj_angle<K, true>(DY2, (unsigned)T, (unsigned)(T >> 32), (unsigned)U.x,
+                                   (unsigned)U.y, step, gs32, h, nrows, acc);
+            }
+        } else {
+            for (int t = 0; t < cnt; ++t) {
+                const longlong2 T2 = s_t[t];
+                const int4 U = s_u[t];
+                const long long snx = ((long long)U.y << 32) | (unsigned)U.x;
+                const float step = __int_as_float(U.z), gs32 = __int_as_float(U.w);
+                const float h = fmaf(-4294967296.0f, gs32, step);
+                const long long T = T2.x + (long long)txc * T2.y - row_off * snx;
+                adj_angle<K, false>(DY2, (unsigned)T, (unsigned)(T >> 32), (unsigned)U.x,
+                                    (unsigned)U.y, step, gs32, h, nrows, acc);
             }
         }
 #pragma unroll
