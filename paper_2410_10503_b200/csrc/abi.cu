@@ -296,7 +296,7 @@ int mct_ray_adjoint(const mct_ray_plan* rp, const float* sino, float* img, int b
     MCT_REQUIRE(rp && sino && img && ws, "null argument");
     MCT_REQUIRE(batch >= 1, "batch must be >= 1");
     cudaStream_t st = (cudaStream_t)stream;
-    MCT_CUDA(launch_pad_sino(sino, static_cast<char*>(ws), rp->item_bytes, rp->off_dy, rp->A, rp->B,
+    MCT_CUDA(launch_pad_sino(sino, rp->d_adj, static_cast<char*>(ws), rp->item_bytes, rp->off_dy, rp->A, rp->B,
                              rp->wy, rp->pb, batch, st),
              "pad sinogram");
     AdjArgs aa = adj_args(rp, ws);
@@ -560,7 +560,7 @@ int mct_gated_adjoint(const mct_family* fam, int slice, int gate, const float* y
     MCT_REQUIRE(slice >= 0 && slice < fam->S && gate >= 0 && gate < fam->N, "gate out of range");
     const mct_ray_plan* rp = fam->ray;
     cudaStream_t st = (cudaStream_t)stream;
-    MCT_CUDA(launch_pad_sino(y, static_cast<char*>(ws), rp->item_bytes, rp->off_dy, rp->A, rp->B,
+    MCT_CUDA(launch_pad_sino(y, rp->d_adj, static_cast<char*>(ws), rp->item_bytes, rp->off_dy, rp->A, rp->B,
                              rp->wy, rp->pb, 1, st),
              "pad sinogram");
     AdjArgs aa = adj_args(rp, ws);

@@ -177,8 +177,9 @@ struct UpdArgs {
 
 // ------------------------------------------------------------- launchers --
 cudaError_t launch_pack(const PackArgs& a, int items, cudaStream_t st);
-cudaError_t launch_pad_sino(const float* sino, char* ws, size_t item_bytes, size_t off_dy, int A,
-                            int B, int wy, int pb, int items, cudaStream_t st);
+cudaError_t launch_pad_sino(const float* sino, const AdjAngle* ang, char* ws, size_t item_bytes,
+                            size_t off_dy, int A, int B, int wy, int pb, int items,
+                            cudaStream_t st);
 cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st);
 cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, cudaStream_t st);
 int choose_asplit(const mct_ray_plan* rp, int items);

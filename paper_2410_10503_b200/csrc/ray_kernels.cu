@@ -87,16 +87,19 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs p) {
     }
 }
 
-// Copy a plain (A, B) sinogram into the pair-packed padded DY2 of each item.
-__global__ void pad_sino_kernel(const float* __restrict__ sino, char* ws, size_t item_bytes,
-                                size_t off_dy, int A, int B, int wy, int pb) {
+// Copy a plain (A, B) sinogram into the pair-packed padded DY2 of each item,
+// pre-scaled by the angle's step length (A^* then only needs the tent weights).
+__global__ void pad_sino_kernel(const float* __restrict__ sino, const AdjAngle* __restrict__ ang,
+                                char* ws, size_t item_bytes, size_t off_dy, int A, int B, int wy,
+                                int pb) {
     const int item = blockIdx.z;
     const int a = blockIdx.y;
+    const float step = ang[a].step;
     float* DY = reinterpret_cast<float*>(ws + (size_t)item * item_bytes + off_dy);
     const float* s = sino + ((long long)item * A + a) * B;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x) {
         const long long e = 2 * ((long long)a * wy + pb + j);
-        const float v = s[j];
+        const float v = s[j] * step;
         DY[e] = v;
         DY[e - 1] = v;
     }
@@ -104,8 +107,8 @@ __global__ void pad_sino_kernel(const float* __restrict__ sino, char* ws, size_t
 
 // ---------------------------------------------------------------------------
 // K2: Joseph forward A (projector.py:201-207 with the weights of :160-183).
-// Block = 8 warps = 8 consecutive angles x 32 consecutive bins: the warps walk
-// nearly the same image lines, so the taps stay L1-resident.
+// Block = 16 warps = 16 consecutive angles x 32 consecutive bins: the warps walk
+// nearly the same image lines, so most taps hit L1.
 // Along the dominant axis the continuous minor index advances by a constant
 // slope.  It is carried in 32.32 fixed point whose integer part also carries
 // the row offset, so one 64-bit add advances both, the integer part is the
@@ -129,10 +132,12 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
     asm("sub.cc.u32 %0, %0, %2;\n\tsubc.u32 %1, %1, %3;" : "+r"(lo), "+r"(hi) : "r"(ilo), "r"(ihi));
 }
 
+#define FWD_ANGLES 16  // warps (= consecutive angles) per block: they share image lines in L1
+
 template <int MODE>
-__global__ void __launch_bounds__(256) fwd_kernel(FwdArgs p) {
+__global__ void __launch_bounds__(32 * FWD_ANGLES) fwd_kernel(FwdArgs p) {
     const int item = blockIdx.z;
-    const int a = blockIdx.y * 8 + threadIdx.y;
+    const int a = blockIdx.y * FWD_ANGLES + threadIdx.y;
     const int j = blockIdx.x * 32 + threadIdx.x;
     if (a >= p.A) return;  // warp-uniform (one angle per warp)
     const bool active = j < p.B;
@@ -254,7 +259,7 @@ __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs p) {
         p.y[off] = yn;
         float* DY = reinterpret_cast<float*>(const_cast<char*>(base) + p.off_dy);
         const long long e = 2 * ((long long)a * p.wy + p.pb + j);
-        const float dlt = yn - yv;
+        const float dlt = (yn - yv) * ra.step;  // pre-scaled for A^* (see K3)
         DY[e] = dlt;
         DY[e - 1] = dlt;
         if (p.proj) p.proj[off] = proj;
@@ -288,27 +293,27 @@ __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs p) {
 
 template <int K, bool FULL>
 __device__ __forceinline__ void adj_angle(const float2* __restrict__ DY2, unsigned tlo,
-                                          unsigned thi, unsigned slo, unsigned shi, float step,
-                                          float gs32, float h, int nrows,
-                                          float (&acc)[ADJ_PPT]) {
+                                          unsigned thi, unsigned slo, unsigned shi, float g32,
+                                          float omg, int nrows, float (&acc)[ADJ_PPT]) {
 #pragma unroll
     for (int m = 0; m < ADJ_PPT; ++m) {
         if (FULL || m < nrows) {
-            // thi = sinogram row base + floor(jc) (>= 0), tlo = frac(jc) * 2^32
+            // thi = sinogram row base + floor(jc) (>= 0), tlo = frac(jc) * 2^32; the
+            // sinogram is pre-scaled by the step, so only the tent weights remain
             const float F = (float)tlo;
             if (K == 0) {
                 const float2 v = __ldg(DY2 + thi);
-                const float w0 = fmaxf(0.0f, fmaf(-F, gs32, step));  // bin floor(jc)
-                const float w1 = fmaxf(0.0f, fmaf(F, gs32, h));      // bin floor(jc) + 1
+                const float w0 = __saturatef(fmaf(-F, g32, 1.0f));  // bin floor(jc)
+                const float w1 = __saturatef(fmaf(F, g32, omg));    // bin floor(jc) + 1
                 acc[m] = fmaf(w0, v.x, fmaf(w1, v.y, acc[m]));
             } else {
                 const float d = F * INV_2_32;
-                const float gs = gs32 * 4294967296.0f;
+                const float g = g32 * 4294967296.0f;
 #pragma unroll
                 for (int mm = -K; mm <= K; mm += 2) {
                     const float2 v = __ldg(DY2 + (int)thi + mm);
-                    const float wa = fmaxf(0.0f, fmaf(-fabsf((float)mm - d), gs, step));
-                    const float wb = fmaxf(0.0f, fmaf(-fabsf((float)(mm + 1) - d), gs, step));
+                    const float wa = __saturatef(fmaf(-fabsf((float)mm - d), g, 1.0f));
+                    const float wb = __saturatef(fmaf(-fabsf((float)(mm + 1) - d), g, 1.0f));
                     acc[m] = fmaf(wa, v.x, fmaf(wb, v.y, acc[m]));
                 }
             }
@@ -320,7 +325,7 @@ __device__ __forceinline__ void adj_angle(const float2* __restrict__ DY2, unsign
 template <int K>
 __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(AdjArgs p) {
     __shared__ longlong2 s_t[ADJ_CH];  // anchor (with sinogram row base), cos/sp
-    __shared__ int4 s_u[ADJ_CH];       // sin/sp (lo, hi), step, step*g*2^-32
+    __shared__ int4 s_u[ADJ_CH];       // sin/sp (lo, hi), g*2^-32, 1 - g
     const int item = blockIdx.z / p.asplit;
     const int split = blockIdx.z - item * p.asplit;
     const int a_beg = (int)((long long)p.A * split / p.asplit);
@@ -350,7 +355,7 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(AdjArgs p) {
                                  ((long long)((a0 + tid) * p.wy + p.pb) << 32);
             s_t[tid] = make_longlong2(TA, aa.csx);
             s_u[tid] = make_int4((int)(unsigned)aa.snx, (int)(aa.snx >> 32),
-                                 __float_as_int(aa.step), __float_as_int(aa.step * aa.g * INV_2_32));
+                                 __float_as_int(aa.g * INV_2_32), __float_as_int(1.0f - aa.g));
         }
         __syncthreads();
         if (nrows <= 0) continue;
@@ -363,22 +368,20 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(AdjArgs p) {
                 const longlong2 T2 = s_t[t];
                 const int4 U = s_u[t];
                 const long long snx = ((long long)U.y << 32) | (unsigned)U.x;
-                const float step = __int_as_float(U.z), gs32 = __int_as_float(U.w);
-                const float h = fmaf(-4294967296.0f, gs32, step);
+                const float g32 = __int_as_float(U.z), omg = __int_as_float(U.w);
                 const long long T = T2.x + (long long)txc * T2.y - row_off * snx;
                 adj_angle<K, true>(DY2, (unsigned)T, (unsigned)(T >> 32), (unsigned)U.x,
-                                   (unsigned)U.y, step, gs32, h, nrows, acc);
+                                   (unsigned)U.y, g32, omg, nrows, acc);
             }
         } else {
             for (int t = 0; t < cnt; ++t) {
                 const longlong2 T2 = s_t[t];
                 const int4 U = s_u[t];
                 const long long snx = ((long long)U.y << 32) | (unsigned)U.x;
-                const float step = __int_as_float(U.z), gs32 = __int_as_float(U.w);
-                const float h = fmaf(-4294967296.0f, gs32, step);
+                const float g32 = __int_as_float(U.z), omg = __int_as_float(U.w);
                 const long long T = T2.x + (long long)txc * T2.y - row_off * snx;
                 adj_angle<K, false>(DY2, (unsigned)T, (unsigned)(T >> 32), (unsigned)U.x,
-                                    (unsigned)U.y, step, gs32, h, nrows, acc);
+                                    (unsigned)U.y, g32, omg, nrows, acc);
             }
         }
 #pragma unroll
@@ -400,15 +403,16 @@ cudaError_t launch_pack(const PackArgs& a, int items, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_pad_sino(const float* sino, char* ws, size_t item_bytes, size_t off_dy, int A,
-                            int B, int wy, int pb, int items, cudaStream_t st) {
+cudaError_t launch_pad_sino(const float* sino, const AdjAngle* ang, char* ws, size_t item_bytes,
+                            size_t off_dy, int A, int B, int wy, int pb, int items,
+                            cudaStream_t st) {
     dim3 block(256), grid((B + 255) / 256, A, items);
-    pad_sino_kernel<<<grid, block, 0, st>>>(sino, ws, item_bytes, off_dy, A, B, wy, pb);
+    pad_sino_kernel<<<grid, block, 0, st>>>(sino, ang, ws, item_bytes, off_dy, A, B, wy, pb);
     return cudaGetLastError();
 }
 
 cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st) {
-    dim3 block(32, 8), grid((a.B + 31) / 32, (a.A + 7) / 8, items);
+    dim3 block(32, FWD_ANGLES), grid((a.B + 31) / 32, (a.A + FWD_ANGLES - 1) / FWD_ANGLES, items);
     if (mode == 0)
         fwd_kernel<0><<<grid, block, 0, st>>>(a);
     else
