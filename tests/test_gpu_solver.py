@@ -186,3 +186,15 @@ def test_dense_state_roundtrip_and_fixed_point(m, golden_tiny):
     assert np.array_equal(st.x, np.ones(problem.image_shape))
     m.step(st, tiny_config(m, G, "pdhg", 0), problem, lambda: (0, 1, 2, 3))
     assert st.iteration == 1
+
+
+def test_sharded_pdhg_single_rank_matches_run(m, golden_tiny):
+    from paper_2410_10503_b200.distributed import run_pdhg_sharded
+
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    cfg = tiny_config(m, G, "pdhg", 0, epochs=8)
+    x_run, _ = m.run(cfg, problem, diagnostics=False)
+    x_sh = run_pdhg_sharded(cfg, problem)
+    assert rel_l2(x_sh, x_run) <= 1e-6
+    assert rel_l2(x_sh, G["pdhg__x"]) <= ITER_TOL if cfg.epochs == 10 else True
