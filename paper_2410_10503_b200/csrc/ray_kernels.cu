@@ -135,7 +135,7 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
 #define FWD_ANGLES 16  // warps (= consecutive angles) per block: they share image lines in L1
 
 template <int MODE>
-__global__ void __launch_bounds__(32 * FWD_ANGLES) fwd_kernel(FwdArgs p) {
+__global__ void __launch_bounds__(32 * FWD_ANGLES, 64 / FWD_ANGLES) fwd_kernel(FwdArgs p) {
     const int item = blockIdx.z;
     const int a = blockIdx.y * FWD_ANGLES + threadIdx.y;
     const int j = blockIdx.x * 32 + threadIdx.x;
@@ -323,7 +323,7 @@ __device__ __forceinline__ void adj_angle(const float2* __restrict__ DY2, unsign
 }
 
 template <int K>
-__global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(AdjArgs p) {
+__global__ void __launch_bounds__(ADJ_THREADS, 12) adj_kernel(AdjArgs p) {
     __shared__ longlong2 s_t[ADJ_CH];  // anchor (with sinogram row base), cos/sp
     __shared__ int4 s_u[ADJ_CH];       // sin/sp (lo, hi), g*2^-32, 1 - g
     const int item = blockIdx.z / p.asplit;
@@ -342,9 +342,11 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(AdjArgs p) {
     const float2* __restrict__ DY2 = reinterpret_cast<const float2*>(base + p.off_dy);
     const long long row_off = (long long)(threadIdx.y * ADJ_PPT);
 
-    double tot[ADJ_PPT];
+    // fp64 running totals live in shared memory (flushed once per 128-angle
+    // chunk) so the registers go to the in-flight loads
+    __shared__ double s_tot[ADJ_PPT][ADJ_THREADS];
 #pragma unroll
-    for (int m = 0; m < ADJ_PPT; ++m) tot[m] = 0.0;
+    for (int m = 0; m < ADJ_PPT; ++m) s_tot[m][tid] = 0.0;
     for (int a0 = a_beg; a0 < a_end; a0 += ADJ_CH) {
         const int cnt = min(ADJ_CH, a_end - a0);
         __syncthreads();
@@ -385,14 +387,14 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(AdjArgs p) {
             }
         }
 #pragma unroll
-        for (int m = 0; m < ADJ_PPT; ++m) tot[m] += (double)acc[m];
+        for (int m = 0; m < ADJ_PPT; ++m) s_tot[m][tid] += (double)acc[m];
     }
     if (c >= p.cols) return;
     float* IMG = reinterpret_cast<float*>(const_cast<char*>(base) + p.off_img +
                                           (size_t)split * p.img_slot_bytes);
 #pragma unroll
     for (int m = 0; m < ADJ_PPT; ++m)
-        if (m < nrows) IMG[(long long)(rt + m) * p.cols + c] = (float)tot[m];
+        if (m < nrows) IMG[(long long)(rt + m) * p.cols + c] = (float)s_tot[m][tid];
 }
 
 }  // namespace
