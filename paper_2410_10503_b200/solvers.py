@@ -472,7 +472,8 @@ class BatchRunner:
         self.problems = list(problems)
         c0 = self.configs[0]
         self.engine = Engine([p.operators for p in problems], [p.data for p in problems],
-                             keep_projections=keep_projections)
+                             keep_projections=keep_projections,
+                             max_items=len(problems) if c0.mode == "spdhg" else None)
         self.engine.set_params(c0)
         self.mode = c0.mode
         self.alpha = problems[0].alpha

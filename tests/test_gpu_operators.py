@@ -139,7 +139,7 @@ def test_forward_adjoint_deterministic(m):
 
 
 # ---------------------------------------------------------------- large sizes
-@pytest.mark.parametrize("n,A,B", [(256, 360, 363), (512, 720, 729)])
+@pytest.mark.parametrize("n,A,B", [(256, 360, 363), (512, 720, 729), (1024, 1440, 1453)])
 def test_ray_parity_vs_oracle_large(m, n, A, B):
     r = np.random.default_rng(n)
     x = r.standard_normal((n, n)).astype(np.float32).astype(np.float64)
@@ -257,3 +257,22 @@ def test_power_method_matches_reference_norms(m, golden_tiny, golden_c1):
     info = m.estimate_norms(m.Geometry(*cfg.geometry_args), inp.gates, iterations=100)
     assert np.allclose(info["gate_norms"], C["gate_norms"], rtol=1e-4)
     assert info["base_norm_sq"] == pytest.approx(float(C["base_norm_sq"]), rel=1e-4)
+
+
+@pytest.mark.parametrize("n,peak", [(512, 6.0), (1024, 8.0)])
+def test_dense_gated_parity_full_size(m, n, peak):
+    """A_i and A_i^* with a BASELINE dense field at C3 / C4 size vs the fp64 oracle."""
+    from paper_2410_10503_b200 import workloads
+
+    A, B = {512: (720, 729), 1024: (1440, 1453)}[n]
+    phi = workloads.bump_field(n, peak, 0, 1)
+    geom = m.Geometry(n, n, A, B, 1.0)
+    op = m.compose(m.ray_transform(geom), m.DenseWarpOperator(phi))
+    orc = oracle.Composed(oracle.RayTransform(oracle.Geometry(n, n, A, B, 1.0),
+                                              threads=oracle.default_threads()),
+                          oracle.Warp((n, n), oracle.DENSE, phi=phi))
+    r = np.random.default_rng(n + 1)
+    x = workloads.ellipse_phantom(n, 12, 5).astype(np.float64)
+    y = r.standard_normal((A, B)).astype(np.float32).astype(np.float64)
+    assert rel_l2(op.apply(x), orc.apply(x)) <= TOL
+    assert rel_l2(op.adjoint_apply(y), orc.adjoint_apply(y)) <= TOL

@@ -198,3 +198,20 @@ def test_sharded_pdhg_single_rank_matches_run(m, golden_tiny):
     x_sh = run_pdhg_sharded(cfg, problem)
     assert rel_l2(x_sh, x_run) <= 1e-6
     assert rel_l2(x_sh, G["pdhg__x"]) <= ITER_TOL if cfg.epochs == 10 else True
+
+
+def test_c2_shape_spdhg_trajectory_vs_oracle(m):
+    """BASELINE C2 shape (256^2, 10 dense gates, 360x363): 2 SPDHG epochs vs the oracle."""
+    from paper_2410_10503_b200 import workloads
+
+    cfgw = workloads.CONFIGS["c2"]
+    problem, truth, inp = m.simulate.workload_problem(cfgw, 0)
+    norms = [m.power_method(op, iterations=20) for op in problem.operators]
+    cfg = m.default_config("spdhg", norms, cfgw.alpha, 2, seed=3)
+    x, rec = m.run(cfg, problem, diagnostics=False)
+    oops = oracle.gate_operators(oracle.Geometry(*cfgw.geometry_args), inp.gates,
+                                 threads=oracle.default_threads())
+    ocfg = osolver.default_config("spdhg", norms, cfgw.alpha, 2, seed=3)
+    st, _ = osolver.run(ocfg, cfgw.alpha, oops, [np.asarray(d) for d in problem.data],
+                        diagnostics=False)
+    assert rel_l2(x, st.x) <= ITER_TOL
