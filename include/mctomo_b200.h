@@ -216,6 +216,15 @@ int mct_reduce(const float* a_dev, const float* b_dev, long long length, int seg
 int mct_axpby(long long n, float alpha, const float* x_dev, float beta, float* y_dev,
               void* stream);
 
+/* Mixed-precision vector ops for the device CG saddle-point solver
+ * (solvers.cg_reference, solvers.py:435-490, GramSumMap linops.py:172-212):
+ * y = alpha*x + beta*y with x, y each fp32 (flag 0) or fp64 (flag 1), fp64
+ * arithmetic; out_dev[0] = sum_i a[i]*b[i] over fp64 vectors (fixed order).   */
+int mct_axpby_mixed(long long n, double alpha, const void* x_dev, int x_is_f64, double beta,
+                    void* y_dev, int y_is_f64, void* stream);
+int mct_dot_f64(const double* a_dev, const double* b_dev, long long n, double* out_dev,
+                void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,6 +16,7 @@ from .motion import DenseWarpOperator, MotionParams, WarpOperator, motion_sequen
 from .projector import Geometry, GatedOperator, RayTransform, adjoint, forward, ray_transform
 from .simulate import estimate_norms, gate_operators, gaussian_field, simulate_data
 from .solvers import (RHO, DivergenceError, Problem, SaddlePoint, SolverConfig, SolverState,
-                      default_config, draw_sequence, run, run_batch, sample_gates, step)
+                      cg_reference, default_config, draw_sequence, optimality_residual, run,
+                      run_batch, sample_gates, step)
 
 __version__ = "0.1.0"

@@ -91,6 +91,9 @@ SIGNATURES = {
     "mct_reduce": (c_int, [c_void_p, c_void_p, c_longlong, c_int, c_longlong, c_int, c_void_p,
                            c_void_p]),
     "mct_axpby": (c_int, [c_longlong, c_float, c_void_p, c_float, c_void_p, c_void_p]),
+    "mct_axpby_mixed": (c_int, [c_longlong, c_double, c_void_p, c_int, c_double, c_void_p, c_int,
+                                c_void_p]),
+    "mct_dot_f64": (c_int, [c_void_p, c_void_p, c_longlong, c_void_p, c_void_p]),
 }
 
 _LIB = None

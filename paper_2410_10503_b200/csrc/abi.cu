@@ -686,4 +686,19 @@ int mct_axpby(long long n, float alpha, const float* x, float beta, float* y, vo
     return MCT_OK;
 }
 
+int mct_axpby_mixed(long long n, double alpha, const void* x, int x_is_f64, double beta, void* y,
+                    int y_is_f64, void* stream) {
+    MCT_REQUIRE(x && y && n >= 0, "null argument");
+    MCT_CUDA(launch_axpby_mixed(n, alpha, x, x_is_f64 ? 1 : 0, beta, y, y_is_f64 ? 1 : 0,
+                                (cudaStream_t)stream),
+             "axpby_mixed");
+    return MCT_OK;
+}
+
+int mct_dot_f64(const double* a, const double* b, long long n, double* out, void* stream) {
+    MCT_REQUIRE(a && b && out && n >= 0, "null argument");
+    MCT_CUDA(launch_dot_f64(a, b, n, out, (cudaStream_t)stream), "dot_f64");
+    return MCT_OK;
+}
+
 }  // extern "C"

@@ -193,6 +193,10 @@ cudaError_t launch_reduce(const float* a, const float* b, long long len, int seg
                           long long stride, int mode, double* out, cudaStream_t st);
 cudaError_t launch_axpby(long long n, float alpha, const float* x, float beta, float* y,
                          cudaStream_t st);
+cudaError_t launch_axpby_mixed(long long n, double alpha, const void* x, int xf64, double beta,
+                               void* y, int yf64, cudaStream_t st);
+cudaError_t launch_dot_f64(const double* a, const double* b, long long n, double* out,
+                           cudaStream_t st);
 cudaError_t launch_absmax(const float* x, long long n, float* out, cudaStream_t st);
 cudaError_t build_dense_transpose(const WarpDesc& desc, int** tptr, int** tidx, float** tw,
                                   long long* nnz, cudaStream_t st);

@@ -180,6 +180,36 @@ __global__ void axpby_kernel(long long n, float alpha, const float* __restrict__
         y[i] = fmaf(alpha, x[i], beta * y[i]);
 }
 
+__global__ void axpby_mixed_kernel(long long n, double alpha, const void* __restrict__ x, int xf64,
+                                   double beta, void* y, int yf64) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double xv = xf64 ? static_cast<const double*>(x)[i] : (double)static_cast<const float*>(x)[i];
+        if (yf64) {
+            double* yp = static_cast<double*>(y);
+            yp[i] = alpha * xv + (beta == 0.0 ? 0.0 : beta * yp[i]);
+        } else {
+            float* yp = static_cast<float*>(y);
+            yp[i] = (float)(alpha * xv + (beta == 0.0 ? 0.0 : beta * (double)yp[i]));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(512) dot_f64_kernel(const double* __restrict__ a,
+                                                      const double* __restrict__ b, long long n,
+                                                      double* out) {
+    __shared__ double sh[512];
+    double acc = 0.0;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) acc += a[i] * b[i];
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
 __global__ void absmax_kernel(const float* __restrict__ x, long long n, float* out) {
     __shared__ float sh[256];
     float m = 0.0f;
@@ -240,6 +270,18 @@ cudaError_t launch_reduce(const float* a, const float* b, long long len, int seg
 cudaError_t launch_axpby(long long n, float alpha, const float* x, float beta, float* y,
                          cudaStream_t st) {
     axpby_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, alpha, x, beta, y);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_axpby_mixed(long long n, double alpha, const void* x, int xf64, double beta,
+                               void* y, int yf64, cudaStream_t st) {
+    axpby_mixed_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, alpha, x, xf64, beta, y, yf64);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dot_f64(const double* a, const double* b, long long n, double* out,
+                           cudaStream_t st) {
+    dot_f64_kernel<<<1, 512, 0, st>>>(a, b, n, out);
     return cudaGetLastError();
 }
 

@@ -294,6 +294,11 @@ class Engine:
                                                  _lib.ptr(x), _lib.ptr(out), _lib.ptr(ws),
                                                  _lib.stream_handle()))
 
+    def gated_adjoint(self, slice_index: int, gate: int, y, out):
+        _lib.check(_lib.load().mct_gated_adjoint(self.family.handle, slice_index, gate,
+                                                 _lib.ptr(y), _lib.ptr(out), _lib.ptr(self.ws),
+                                                 _lib.stream_handle()))
+
     def objectives(self, alpha: float, reuse_projections: bool):
         """Per-slice objective alpha||x||^2 + sum_i ||A_i x - d_i||^2 / N (fp64)."""
         torch = self.torch

@@ -28,7 +28,8 @@ from mctomo.motion import MotionParams, WarpOperator, motion_sequence  # noqa: E
 from mctomo.projector import Geometry, ray_transform  # noqa: E402
 from mctomo.simulate import (estimate_norms, gate_operators, gaussian_field,  # noqa: E402
                              generate, make_phantom)
-from mctomo.solvers import Problem, default_config, run, sample_gates  # noqa: E402
+from mctomo.solvers import (Problem, cg_reference, default_config, optimality_residual,  # noqa: E402
+                            run, sample_gates)
 
 from paper_2410_10503_b200 import workloads  # noqa: E402  (numpy-only input generators)
 
@@ -125,6 +126,11 @@ def solver_tiny():
         "base_norm_sq": np.array(norms["base_norm_sq"]),
         "alpha": np.array(alpha),
     }
+    saddle = cg_reference(problem, tol=1e-13, max_iter=3000)
+    out["saddle_x"] = saddle.x_star
+    out["saddle_y"] = np.stack(saddle.y_star)
+    out["saddle_residual"] = np.array(saddle.residual)
+    out["saddle_optimality"] = np.array(optimality_residual(problem, saddle))
     for mode, seed in (("pdhg", 0), ("spdhg", 5)):
         cfg = default_config(mode, norms["gate_norms"], alpha, epochs=10, seed=seed,
                              stacked_norm_sq=norms["stacked_norm_sq"] if mode == "pdhg" else None)
@@ -133,7 +139,8 @@ def solver_tiny():
         def grab(e, s, states=states):
             states[e] = (s.x.copy(), [v.copy() for v in s.y], s.z.copy(), s.zbar.copy())
 
-        x, rec = run(cfg, problem, truth=phantom, on_epoch=grab)
+        x, rec = run(cfg, problem, saddle=saddle, truth=phantom, on_epoch=grab)
+        out[f"{mode}__dist_sq"] = np.array(rec.dist_sq)
         out[f"{mode}__x"] = x
         out[f"{mode}__y"] = np.stack(states[10][1])
         out[f"{mode}__z"] = states[10][2]

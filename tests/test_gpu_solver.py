@@ -215,3 +215,25 @@ def test_c2_shape_spdhg_trajectory_vs_oracle(m):
     st, _ = osolver.run(ocfg, cfgw.alpha, oops, [np.asarray(d) for d in problem.data],
                         diagnostics=False)
     assert rel_l2(x, st.x) <= ITER_TOL
+
+
+def test_cg_reference_matches_reference_saddle(m, golden_tiny):
+    """Device CG saddle (solvers.py:435-490) vs the reference's fp64 CG saddle."""
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    sp = m.cg_reference(problem, tol=1e-6, max_iter=2000)
+    assert sp.converged and sp.source == "cg_reference"
+    assert sp.residual <= 1e-5
+    assert rel_l2(sp.x_star, G["saddle_x"]) <= 1e-4
+    assert rel_l2(np.stack(sp.y_star), G["saddle_y"]) <= 1e-4
+    assert m.optimality_residual(problem, sp) <= 1e-4 * max(1.0, np.linalg.norm(sp.x_star))
+    # the reference's saddle drives run()'s dist_sq column (solvers.py:407)
+    ref = m.SaddlePoint(x_star=G["saddle_x"], y_star=list(G["saddle_y"]), source="reference",
+                        converged=True, residual=float(G["saddle_residual"]))
+    for mode, seed in (("pdhg", 0), ("spdhg", 5)):
+        _, rec = m.run(tiny_config(m, G, mode, seed), problem, saddle=ref)
+        assert np.allclose(rec.dist_sq, G[f"{mode}__dist_sq"], rtol=ITER_TOL)
+    tight = m.cg_reference(problem, tol=1e-13, max_iter=3)
+    assert not tight.converged
+    with pytest.raises(ValueError):
+        m.cg_reference(problem, tol=0.0)
