@@ -422,14 +422,26 @@ cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// Angle split of A^*: fill one wave of resident blocks when a launch has few
+// tiles (single-gate SPDHG), never exceeding it (a partial second wave would
+// idle most SMs); every split keeps >= 16 angles.
 int choose_asplit(const mct_ray_plan* rp, int items) {
+    static int slots = 0;  // resident adj blocks per GPU (queried once)
+    if (slots == 0) {
+        int dev = 0, sms = 148, per_sm = 8;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_kernel<0>, ADJ_THREADS, 0) !=
+                cudaSuccess || per_sm < 1)
+            per_sm = 8;
+        slots = sms * per_sm;
+    }
     const long long tiles = (long long)((rp->cols + ADJ_TW - 1) / ADJ_TW) *
                             ((rp->rows + ADJ_TH - 1) / ADJ_TH) * (items > 0 ? items : 1);
-    const long long target = 148LL * 8;  // >= 8 resident blocks per SM
-    long long s = (target + tiles - 1) / tiles;
+    long long s = tiles >= slots ? 1 : slots / tiles;
     s = s < 1 ? 1 : s;
     s = s > MCT_MAX_ASPLIT ? MCT_MAX_ASPLIT : s;
-    const long long by_angles = rp->A / 16 > 0 ? rp->A / 16 : 1;  // >= 16 angles per split
+    const long long by_angles = rp->A / 16 > 0 ? rp->A / 16 : 1;
     return (int)(s < by_angles ? s : by_angles);
 }
 
