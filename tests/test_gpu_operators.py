@@ -276,3 +276,41 @@ def test_dense_gated_parity_full_size(m, n, peak):
     y = r.standard_normal((A, B)).astype(np.float32).astype(np.float64)
     assert rel_l2(op.apply(x), orc.apply(x)) <= TOL
     assert rel_l2(op.adjoint_apply(y), orc.adjoint_apply(y)) <= TOL
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("g", [
+    (1, 1, 1, 1, 1.0),          # single pixel, single ray
+    (7, 3, 5, 4, 0.8),          # ragged, few bins
+    (50, 20, 13, 9, 2.5),       # detector narrower than the image (rays miss corners)
+    (32, 32, 7, 200, 0.3),      # fine bins: wide adjoint footprint (K = 3)
+    (19, 41, 64, 61, 1.0),      # non-square, 45-degree tie handled by the host flags
+])
+def test_edge_geometries_vs_oracle(m, g):
+    r = np.random.default_rng(sum(int(v) for v in g[:4]))
+    geom = m.Geometry(*g)
+    op = m.RayTransform(geom)
+    orc = oracle.RayTransform(oracle.Geometry(*g))
+    x = r.standard_normal(geom.image_shape).astype(np.float32).astype(np.float64)
+    y = r.standard_normal(geom.sino_shape).astype(np.float32).astype(np.float64)
+    assert rel_l2(op.apply(x), orc.apply(x)) <= TOL
+    assert rel_l2(op.adjoint_apply(y), orc.adjoint_apply(y)) <= TOL
+
+
+def test_too_fine_detector_rejected(m):
+    with pytest.raises(ValueError, match="spacing"):
+        m.RayTransform(m.Geometry(32, 32, 8, 400, 0.1)).apply(np.zeros((32, 32)))
+
+
+def test_dense_zero_field_is_identity_and_out_of_frame(m, rng):
+    x = rng.standard_normal((40, 33)).astype(np.float32).astype(np.float64)
+    w0 = m.DenseWarpOperator(np.zeros((2, 40, 33), dtype=np.float32))
+    assert np.array_equal(w0.apply(x), x)
+    assert np.array_equal(w0.adjoint_apply(x), x)
+    far = np.full((2, 40, 33), 500.0, dtype=np.float32)
+    wf = m.DenseWarpOperator(far)
+    assert np.all(wf.apply(x) == 0.0) and np.all(wf.adjoint_apply(x) == 0.0)
+    with pytest.raises(ValueError):
+        m.DenseWarpOperator(np.full((2, 4, 4), np.nan, dtype=np.float32))
+    with pytest.raises(ValueError):
+        m.DenseWarpOperator(np.zeros((3, 4, 4)))

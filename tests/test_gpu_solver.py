@@ -239,3 +239,31 @@ def test_cg_reference_matches_reference_saddle(m, golden_tiny):
     assert not tight.converged
     with pytest.raises(ValueError):
         m.cg_reference(problem, tol=0.0)
+
+
+def test_single_gate_and_uncompensated(m):
+    """N = 1 (SPDHG == PDHG step rules) and compensated=False (the no-MC baseline)."""
+    from paper_2410_10503_b200 import workloads
+
+    geom = m.Geometry(48, 48, 40, 69, 1.0)
+    truth = workloads.ellipse_phantom(48, 5, 9)
+    gates = workloads.rigid_gates(3, 9)
+    ops_mc = m.gate_operators(geom, gates, compensated=True)
+    ops_no = m.gate_operators(geom, gates, compensated=False)
+    assert all(op is m.ray_transform(geom) for op in ops_no)
+    data = m.simulate_data(ops_mc, truth, 9)
+    one = m.Problem.from_parts(1e-2, ops_mc[:1], data[:1])
+    nrm = [m.power_method(ops_mc[0], iterations=30)]
+    x1, _ = m.run(m.default_config("pdhg", nrm, 1e-2, 5), one)
+    oops = oracle.gate_operators(oracle.Geometry(48, 48, 40, 69, 1.0), gates[:1])
+    st, _ = osolver.run(osolver.default_config("pdhg", nrm, 1e-2, 5), 1e-2, oops, data[:1],
+                        diagnostics=False)
+    assert rel_l2(x1, st.x) <= ITER_TOL
+    nomc = m.Problem.from_parts(1e-2, ops_no, data)
+    norms = [m.power_method(op, iterations=30) for op in ops_no]
+    xn, rec = m.run(m.default_config("spdhg", norms, 1e-2, 3, seed=2), nomc)
+    o_no = [oracle.RayTransform(oracle.Geometry(48, 48, 40, 69, 1.0))] * 3
+    st, objs = osolver.run(osolver.default_config("spdhg", norms, 1e-2, 3, seed=2), 1e-2, o_no,
+                           data)
+    assert rel_l2(xn, st.x) <= ITER_TOL
+    assert np.allclose(rec.objective, objs, rtol=ITER_TOL)
