@@ -132,7 +132,7 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
     asm("sub.cc.u32 %0, %0, %2;\n\tsubc.u32 %1, %1, %3;" : "+r"(lo), "+r"(hi) : "r"(ilo), "r"(ihi));
 }
 
-#define FWD_ANGLES 16  // warps (= consecutive angles) per block: they share image lines in L1
+#define FWD_ANGLES 4  // warps (= consecutive angles) per block: they share image lines in L1
 
 template <int MODE>
 __global__ void __launch_bounds__(32 * FWD_ANGLES, 64 / FWD_ANGLES) fwd_kernel(FwdArgs p) {
