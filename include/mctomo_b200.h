@@ -209,8 +209,12 @@ int mct_epoch_advance(int32_t* epoch_ctr_dev, int32_t increment, void* stream);
  * out_dev[s] = sum_i (a[s*stride+i]-b[s*stride+i])^2      (mode 1; b NULL -> a^2) */
 #define MCT_REDUCE_DOT 0
 #define MCT_REDUCE_SQDIFF 1
+/* scratch_dev (optional, >= segments*MCT_REDUCE_PARTS doubles) enables the
+ * two-pass multi-block reduction (same fixed order, still bitwise reproducible);
+ * with NULL one block per segment does all the work.                          */
+#define MCT_REDUCE_PARTS 128
 int mct_reduce(const float* a_dev, const float* b_dev, long long length, int segments,
-               long long stride, int mode, double* out_dev, void* stream);
+               long long stride, int mode, double* out_dev, double* scratch_dev, void* stream);
 
 /* y = alpha*x + beta*y elementwise (fp32; used by the device power iteration). */
 int mct_axpby(long long n, float alpha, const float* x_dev, float beta, float* y_dev,
@@ -223,7 +227,7 @@ int mct_axpby(long long n, float alpha, const float* x_dev, float beta, float* y
 int mct_axpby_mixed(long long n, double alpha, const void* x_dev, int x_is_f64, double beta,
                     void* y_dev, int y_is_f64, void* stream);
 int mct_dot_f64(const double* a_dev, const double* b_dev, long long n, double* out_dev,
-                void* stream);
+                double* scratch_dev, void* stream);
 
 #ifdef __cplusplus
 }

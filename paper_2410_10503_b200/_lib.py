@@ -89,11 +89,11 @@ SIGNATURES = {
     "mct_iter_z_update": (c_int, [c_void_p, ctypes.POINTER(State), c_void_p, c_double, c_void_p]),
     "mct_epoch_advance": (c_int, [c_void_p, c_int32, c_void_p]),
     "mct_reduce": (c_int, [c_void_p, c_void_p, c_longlong, c_int, c_longlong, c_int, c_void_p,
-                           c_void_p]),
+                           c_void_p, c_void_p]),
     "mct_axpby": (c_int, [c_longlong, c_float, c_void_p, c_float, c_void_p, c_void_p]),
     "mct_axpby_mixed": (c_int, [c_longlong, c_double, c_void_p, c_int, c_double, c_void_p, c_int,
                                 c_void_p]),
-    "mct_dot_f64": (c_int, [c_void_p, c_void_p, c_longlong, c_void_p, c_void_p]),
+    "mct_dot_f64": (c_int, [c_void_p, c_void_p, c_longlong, c_void_p, c_void_p, c_void_p]),
 }
 
 _LIB = None
@@ -151,3 +151,20 @@ def stream_handle(stream=None) -> int:
 
 def ptr(t) -> int:
     return int(t.data_ptr())
+
+
+REDUCE_PARTS = 128
+_SCRATCH = {}
+
+
+def scratch(device, segments: int = 1):
+    """Cached fp64 scratch for the two-pass reductions (per device and stream, so
+    reductions issued on different streams never share partials)."""
+    import torch
+
+    key = (str(device), stream_handle())
+    need = REDUCE_PARTS * max(1, segments)
+    t = _SCRATCH.get(key)
+    if t is None or t.numel() < need:
+        t = _SCRATCH[key] = torch.empty(need, dtype=torch.float64, device=device)
+    return t

@@ -672,11 +672,12 @@ int mct_epoch_advance(int32_t* ctr, int32_t inc, void* stream) {
 
 // -------------------------------------------------------------- reductions
 int mct_reduce(const float* a, const float* b, long long length, int segments, long long stride,
-               int mode, double* out, void* stream) {
+               int mode, double* out, double* scratch, void* stream) {
     MCT_REQUIRE(a && out, "null argument");
     MCT_REQUIRE(length >= 0 && segments >= 1, "invalid reduction shape");
     MCT_REQUIRE(mode == MCT_REDUCE_DOT || mode == MCT_REDUCE_SQDIFF, "invalid reduction mode");
-    MCT_CUDA(launch_reduce(a, b, length, segments, stride, mode, out, (cudaStream_t)stream), "reduce");
+    MCT_CUDA(launch_reduce(a, b, length, segments, stride, mode, out, scratch, (cudaStream_t)stream),
+             "reduce");
     return MCT_OK;
 }
 
@@ -695,9 +696,10 @@ int mct_axpby_mixed(long long n, double alpha, const void* x, int x_is_f64, doub
     return MCT_OK;
 }
 
-int mct_dot_f64(const double* a, const double* b, long long n, double* out, void* stream) {
+int mct_dot_f64(const double* a, const double* b, long long n, double* out, double* scratch,
+                void* stream) {
     MCT_REQUIRE(a && b && out && n >= 0, "null argument");
-    MCT_CUDA(launch_dot_f64(a, b, n, out, (cudaStream_t)stream), "dot_f64");
+    MCT_CUDA(launch_dot_f64(a, b, n, out, scratch, (cudaStream_t)stream), "dot_f64");
     return MCT_OK;
 }
 

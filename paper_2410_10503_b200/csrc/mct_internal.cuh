@@ -190,13 +190,14 @@ cudaError_t launch_epoch_advance(int* ctr, int inc, cudaStream_t st);
 cudaError_t launch_warp_fwd_plain(const WarpDesc* d_desc, const float* x, float* out, int rows,
                                   int cols, cudaStream_t st);
 cudaError_t launch_reduce(const float* a, const float* b, long long len, int segs,
-                          long long stride, int mode, double* out, cudaStream_t st);
+                          long long stride, int mode, double* out, double* scratch,
+                          cudaStream_t st);
 cudaError_t launch_axpby(long long n, float alpha, const float* x, float beta, float* y,
                          cudaStream_t st);
 cudaError_t launch_axpby_mixed(long long n, double alpha, const void* x, int xf64, double beta,
                                void* y, int yf64, cudaStream_t st);
 cudaError_t launch_dot_f64(const double* a, const double* b, long long n, double* out,
-                           cudaStream_t st);
+                           double* scratch, cudaStream_t st);
 cudaError_t launch_absmax(const float* x, long long n, float* out, cudaStream_t st);
 cudaError_t build_dense_transpose(const WarpDesc& desc, int** tptr, int** tidx, float** tw,
                                   long long* nnz, cudaStream_t st);

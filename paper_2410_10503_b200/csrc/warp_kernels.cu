@@ -145,32 +145,66 @@ __global__ void dense_sort_kernel(long long n, const int* tptr, int* tidx, float
 }
 
 // ------------------------------------------------------------ reductions --
-// One block per segment, fixed thread->element map and fixed tree: the fp64
-// result is bitwise reproducible run to run.
-__global__ void __launch_bounds__(512) reduce_kernel(const float* __restrict__ a,
-                                                     const float* __restrict__ b, long long len,
-                                                     long long stride, int mode, double* out) {
-    __shared__ double sh[512];
-    const int s = blockIdx.x;
-    const float* as = a + (long long)s * stride;
-    const float* bs = b ? b + (long long)s * stride : nullptr;
-    double acc = 0.0;
-    for (long long i = threadIdx.x; i < len; i += blockDim.x) {
-        double x = (double)as[i];
-        if (mode == MCT_REDUCE_DOT) {
-            acc += x * (double)(bs ? bs[i] : 1.0f);
-        } else {
-            double d = bs ? x - (double)bs[i] : x;
-            acc += d * d;
-        }
-    }
+// Fixed thread->element map and fixed trees: the fp64 result is bitwise
+// reproducible run to run.  Pass 1: `parts` blocks per segment, each a
+// contiguous chunk; pass 2 (parts > 1): one block sums the partials in order.
+template <typename T>
+__device__ __forceinline__ double block_sum(double acc, T* sh) {
     sh[threadIdx.x] = acc;
     __syncthreads();
     for (int w = blockDim.x / 2; w > 0; w >>= 1) {
         if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
         __syncthreads();
     }
-    if (threadIdx.x == 0) out[s] = sh[0];
+    return sh[0];
+}
+
+__global__ void __launch_bounds__(256) reduce_kernel(const float* __restrict__ a,
+                                                     const float* __restrict__ b, long long len,
+                                                     long long stride, int mode, int parts,
+                                                     double* out) {
+    __shared__ double sh[256];
+    const int s = blockIdx.y, part = blockIdx.x;
+    const long long chunk = (len + parts - 1) / parts;
+    const long long lo = part * chunk, hi = min(len, lo + chunk);
+    const float* as = a + (long long)s * stride;
+    const float* bs = b ? b + (long long)s * stride : nullptr;
+    double acc = 0.0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double x = (double)__ldg(as + i);
+        if (mode == MCT_REDUCE_DOT) {
+            acc += x * (double)(bs ? __ldg(bs + i) : 1.0f);
+        } else {
+            const double d = bs ? x - (double)__ldg(bs + i) : x;
+            acc += d * d;
+        }
+    }
+    const double r = block_sum(acc, sh);
+    if (threadIdx.x == 0) out[(long long)s * parts + part] = r;
+}
+
+__global__ void __launch_bounds__(256) dot_f64_kernel(const double* __restrict__ a,
+                                                      const double* __restrict__ b, long long len,
+                                                      int parts, double* out) {
+    __shared__ double sh[256];
+    const int part = blockIdx.x;
+    const long long chunk = (len + parts - 1) / parts;
+    const long long lo = part * chunk, hi = min(len, lo + chunk);
+    double acc = 0.0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) acc += a[i] * (b ? b[i] : 1.0);
+    const double r = block_sum(acc, sh);
+    if (threadIdx.x == 0) out[part] = r;
+}
+
+// sum `parts` consecutive partials of each segment, in order
+__global__ void __launch_bounds__(256) partials_kernel(const double* __restrict__ part_in,
+                                                       int parts, double* out) {
+    __shared__ double sh[256];
+    const int s = blockIdx.x;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < parts; i += blockDim.x) acc += part_in[(long long)s * parts + i];
+    const double r = block_sum(acc, sh);
+    if (threadIdx.x == 0) out[s] = r;
 }
 
 __global__ void axpby_kernel(long long n, float alpha, const float* __restrict__ x, float beta,
@@ -193,21 +227,6 @@ __global__ void axpby_mixed_kernel(long long n, double alpha, const void* __rest
             yp[i] = (float)(alpha * xv + (beta == 0.0 ? 0.0 : beta * (double)yp[i]));
         }
     }
-}
-
-__global__ void __launch_bounds__(512) dot_f64_kernel(const double* __restrict__ a,
-                                                      const double* __restrict__ b, long long n,
-                                                      double* out) {
-    __shared__ double sh[512];
-    double acc = 0.0;
-    for (long long i = threadIdx.x; i < n; i += blockDim.x) acc += a[i] * b[i];
-    sh[threadIdx.x] = acc;
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *out = sh[0];
 }
 
 __global__ void absmax_kernel(const float* __restrict__ x, long long n, float* out) {
@@ -261,9 +280,20 @@ cudaError_t launch_warp_fwd_plain(const WarpDesc* d_desc, const float* x, float*
     return cudaGetLastError();
 }
 
+static int reduce_parts(long long len) {
+    long long p = (len + 8191) / 8192;  // >= 8K elements per block
+    return (int)(p < 1 ? 1 : (p > MCT_REDUCE_PARTS ? MCT_REDUCE_PARTS : p));
+}
+
 cudaError_t launch_reduce(const float* a, const float* b, long long len, int segs, long long stride,
-                          int mode, double* out, cudaStream_t st) {
-    reduce_kernel<<<segs, 512, 0, st>>>(a, b, len, stride, mode, out);
+                          int mode, double* out, double* scratch, cudaStream_t st) {
+    const int parts = scratch ? reduce_parts(len) : 1;
+    if (parts == 1) {
+        reduce_kernel<<<dim3(1, segs), 256, 0, st>>>(a, b, len, stride, mode, 1, out);
+        return cudaGetLastError();
+    }
+    reduce_kernel<<<dim3(parts, segs), 256, 0, st>>>(a, b, len, stride, mode, parts, scratch);
+    partials_kernel<<<segs, 256, 0, st>>>(scratch, parts, out);
     return cudaGetLastError();
 }
 
@@ -280,8 +310,14 @@ cudaError_t launch_axpby_mixed(long long n, double alpha, const void* x, int xf6
 }
 
 cudaError_t launch_dot_f64(const double* a, const double* b, long long n, double* out,
-                           cudaStream_t st) {
-    dot_f64_kernel<<<1, 512, 0, st>>>(a, b, n, out);
+                           double* scratch, cudaStream_t st) {
+    const int parts = scratch ? reduce_parts(n) : 1;
+    if (parts == 1) {
+        dot_f64_kernel<<<1, 256, 0, st>>>(a, b, n, 1, out);
+        return cudaGetLastError();
+    }
+    dot_f64_kernel<<<parts, 256, 0, st>>>(a, b, n, parts, scratch);
+    partials_kernel<<<1, 256, 0, st>>>(scratch, parts, out);
     return cudaGetLastError();
 }
 

@@ -285,6 +285,7 @@ class Engine:
         out = self.torch.empty(segments, dtype=self.torch.float64, device=self.device)
         _lib.check(_lib.load().mct_reduce(_lib.ptr(a), _lib.ptr(b) if b is not None else None,
                                           length, segments, length, mode, _lib.ptr(out),
+                                          _lib.ptr(_lib.scratch(self.device, segments)),
                                           _lib.stream_handle()))
         return out
 

@@ -50,7 +50,8 @@ def device_dot(a, b=None, mode: int = _lib.REDUCE_DOT) -> float:
     out = torch.empty(1, dtype=torch.float64, device=a.device)
     bp = _lib.ptr(b) if b is not None else None
     _lib.check(_lib.load().mct_reduce(_lib.ptr(a), bp, a.numel(), 1, a.numel(), mode,
-                                      _lib.ptr(out), _lib.stream_handle()))
+                                      _lib.ptr(out), _lib.ptr(_lib.scratch(a.device)),
+                                      _lib.stream_handle()))
     return float(out.item())
 
 

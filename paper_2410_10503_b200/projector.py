@@ -132,8 +132,20 @@ class RayTransform(LinearMap):
         return p
 
     def workspace(self, items: int):
+        """Zeroed workspace for `items` items, cached per (device, stream).
+
+        The kernels overwrite every interior element they read and never write
+        the zero pads, so a workspace can be reused by any later call issued on
+        the same stream (calls on other streams get their own buffer).
+        """
         torch = _lib.require_cuda()
-        return torch.zeros(self.plan().item_bytes * items, dtype=torch.uint8, device="cuda")
+        need = self.plan().item_bytes * items
+        cache = self.__dict__.setdefault("_ws", {})
+        key = (torch.cuda.current_device(), _lib.stream_handle())
+        ws = cache.get(key)
+        if ws is None or ws.numel() < need:
+            ws = cache[key] = torch.zeros(need, dtype=torch.uint8, device="cuda")
+        return ws
 
     def forward_batch(self, x):
         """A on a (batch, rows, cols) fp32 CUDA tensor -> (batch, A, B)."""

@@ -536,7 +536,9 @@ class _DeviceGram:
 
     def dot(self, a, b) -> float:
         _lib.check(_lib.load().mct_dot_f64(_lib.ptr(a), _lib.ptr(b), a.numel(),
-                                            _lib.ptr(self.dot_out), _lib.stream_handle()))
+                                            _lib.ptr(self.dot_out),
+                                            _lib.ptr(_lib.scratch(a.device)),
+                                            _lib.stream_handle()))
         return float(self.dot_out.item())
 
     def rhs(self, out):

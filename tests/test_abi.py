@@ -67,6 +67,6 @@ def test_null_arguments_rejected():
     with pytest.raises(ValueError):
         _lib.check(L.mct_ray_forward(None, None, None, 1, None, None))
     with pytest.raises(ValueError):
-        _lib.check(L.mct_reduce(None, None, 10, 1, 10, 0, None, None))
+        _lib.check(L.mct_reduce(None, None, 10, 1, 10, 0, None, None, None))
     with pytest.raises(ValueError):
         _lib.check(L.mct_warp_plan_create_dilatation(ctypes.byref(ctypes.c_void_p()), 4, 4, 0.0))
