@@ -18,7 +18,9 @@ for r in rows[2:]:
     for k in ('dram__bytes_read.sum', 'dram__bytes_write.sum'):
         i = hdr.index(k)
         tot += float(r[i].replace(',', '')) * scale[units[i]]
-    key = 'K2_forward_dual' if 'fwd_kernel' in name else 'K3_adjoint' if 'adj_kernel' in name else name
+    key = ('K2_forward_dual' if 'fwd_kernel' in name else 'K3_adjoint' if 'adj_kernel' in name
+           else 'K1_prox_warp' if 'pack_kernel' in name else 'K4_adjoint_update'
+           if 'update_kernel' in name else name)
     out[key] = tot
 out['source'] = Path(rep).name + ' (C3, 20-item PDHG launch, ncu --set full --clock-control none)'
 Path('profiles').mkdir(exist_ok=True)
