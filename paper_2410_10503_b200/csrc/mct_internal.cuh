@@ -52,8 +52,17 @@ struct mct_ray_plan {
     int has_rows, has_cols;
     RayAngle* d_fwd;
     AdjAngle* d_adj;
-    size_t off_x, off_xt, off_dy, off_img, img_slot_bytes, item_bytes;
+    size_t off_x, off_xt, off_dy, off_img, img_slot_bytes, off_part, off_cnt, item_bytes;
 };
+
+// K2 may split every ray's sample walk into ksplit <= MCT_KSPLIT consecutive
+// parts handled by different blocks (shorter blocks -> better load balance of
+// single-gate SPDHG launches); the last block of a tile to finish sums the fp64
+// partials in part order and runs the epilogue.  ksplit = 2 exactly when a
+// launch carries one gate per slice, so a batch of slices and a single slice
+// (or PDHG and a full-draw SPDHG step) run bitwise-identical arithmetic.
+#define MCT_KSPLIT 2
+#define MCT_FWD_ANGLES 4
 
 // --------------------------------------------------------------- warp plan --
 struct WarpDesc {
@@ -133,7 +142,8 @@ struct FwdArgs {
     int A, B, rows, cols, wx, wxt;
     double sp, jmid;
     const char* ws;
-    size_t item_bytes, off_x, off_xt, off_dy;
+    size_t item_bytes, off_x, off_xt, off_dy, off_part, off_cnt;
+    int ksplit;
     int wy, pb;
     ItemSel sel;
     int N;

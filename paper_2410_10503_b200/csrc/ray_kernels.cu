@@ -132,15 +132,18 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
     asm("sub.cc.u32 %0, %0, %2;\n\tsubc.u32 %1, %1, %3;" : "+r"(lo), "+r"(hi) : "r"(ilo), "r"(ihi));
 }
 
-#define FWD_ANGLES 4  // warps (= consecutive angles) per block: they share image lines in L1
+#define FWD_ANGLES MCT_FWD_ANGLES  // warps (= consecutive angles) per block; they share L1 lines
 
 template <int MODE>
 __global__ void __launch_bounds__(32 * FWD_ANGLES, 64 / FWD_ANGLES) fwd_kernel(FwdArgs p) {
-    const int item = blockIdx.z;
-    const int a = blockIdx.y * FWD_ANGLES + threadIdx.y;
+    const int ks = p.ksplit;
+    const int item = blockIdx.z / ks;
+    const int part = blockIdx.z - item * ks;
+    const int a_raw = blockIdx.y * FWD_ANGLES + threadIdx.y;
+    const bool warp_on = a_raw < p.A;        // warp-uniform; no early exit (block syncs below)
+    const int a = warp_on ? a_raw : p.A - 1;
     const int j = blockIdx.x * 32 + threadIdx.x;
-    if (a >= p.A) return;  // warp-uniform (one angle per warp)
-    const bool active = j < p.B;
+    const bool active = warp_on && j < p.B;
     const int jj = active ? j : p.B - 1;  // idle lanes shadow the last bin (no store)
     const RayAngle ra = p.ang[a];
     const char* base = p.ws + (size_t)item * p.item_bytes;
@@ -167,12 +170,20 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, 64 / FWD_ANGLES) fwd_kernel(F
         lo = max(0, (int)floor(kmin));
         hi = min(nmaj - 1, (int)ceil(kmax));
     }
-    const int wlo = __reduce_min_sync(0xffffffffu, lo);  // union of the warp's ranges
-    const int whi = __reduce_max_sync(0xffffffffu, hi);
+    int wlo = __reduce_min_sync(0xffffffffu, lo);  // union of the warp's ranges
+    int whi = __reduce_max_sync(0xffffffffu, hi);
     int clo = __reduce_max_sync(0xffffffffu, lo);        // common core
     int chi = __reduce_min_sync(0xffffffffu, hi);
-    float acc = 0.0f;
-    if (wlo <= whi) {
+    // this block's share of the walk: part `part` of ks equal pieces
+    const int wlen = whi - wlo + 1;
+    const int k_lo = wlo + (int)((long long)wlen * part / ks);
+    const int k_hi = wlo + (int)((long long)wlen * (part + 1) / ks) - 1;
+    wlo = k_lo;
+    whi = k_hi;
+    clo = max(clo, k_lo);
+    chi = min(chi, k_hi);
+    double tot = 0.0;
+    if (warp_on && wlo <= whi) {
         if (clo > chi) { clo = whi + 1; chi = whi; }     // no common core: all edge
         const long long inc64 = ra.slope_fx + ((long long)stride << 32);
         const unsigned ilo = (unsigned)inc64, ihi = (unsigned)(inc64 >> 32);
@@ -242,10 +253,32 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, 64 / FWD_ANGLES) fwd_kernel(F
             fx_add(flo, fhi, ilo, ihi);
             rowoff += stride;
         }
-        acc = (float)(dacc + (double)ea);
+        tot = dacc + (double)ea;
     }
-    const float proj = acc * ra.step;
-    if (!active) return;
+    double sum = tot;
+    if (ks > 1) {
+        // combine the parts: the last block of this tile to arrive sums them in order
+        double* PART = reinterpret_cast<double*>(const_cast<char*>(base) + p.off_part);
+        if (active) PART[((long long)part * p.A + a) * p.B + j] = tot;
+        __shared__ int s_last;
+        __syncthreads();
+        if (threadIdx.x == 0 && threadIdx.y == 0) {
+            __threadfence();
+            int* cnt = reinterpret_cast<int*>(const_cast<char*>(base) + p.off_cnt) +
+                       blockIdx.y * gridDim.x + blockIdx.x;
+            const int prev = atomicAdd(cnt, 1);
+            s_last = (prev == ks - 1);
+            if (s_last) *cnt = 0;  // every part has arrived: re-arm for the next launch
+        }
+        __syncthreads();
+        if (!s_last || !active) return;
+        __threadfence();
+        sum = 0.0;
+        for (int q = 0; q < ks; ++q) sum += __ldcg(PART + ((long long)q * p.A + a) * p.B + j);
+    } else if (!active) {
+        return;
+    }
+    const float proj = (float)sum * ra.step;
     if (MODE == 0) {
         p.out[(long long)item * p.out_item_stride + (long long)a * p.B + j] = proj;
     } else {
@@ -414,7 +447,8 @@ cudaError_t launch_pad_sino(const float* sino, const AdjAngle* ang, char* ws, si
 }
 
 cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st) {
-    dim3 block(32, FWD_ANGLES), grid((a.B + 31) / 32, (a.A + FWD_ANGLES - 1) / FWD_ANGLES, items);
+    dim3 block(32, FWD_ANGLES),
+        grid((a.B + 31) / 32, (a.A + FWD_ANGLES - 1) / FWD_ANGLES, items * a.ksplit);
     if (mode == 0)
         fwd_kernel<0><<<grid, block, 0, st>>>(a);
     else
