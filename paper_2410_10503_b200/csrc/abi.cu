@@ -319,6 +319,18 @@ int mct_ray_adjoint(const mct_ray_plan* rp, const float* sino, float* img, int b
 }
 
 // ----------------------------------------------------------------- warps
+// Transposed gather list of a non-identity warp (the adjoint D^* reads it): built
+// on the device from the forward's own taps, so forward and adjoint weights are
+// bit-identical.  Synchronous (plan construction only).
+static cudaError_t attach_transpose(mct_warp_plan* p, cudaStream_t st) {
+    cudaError_t e = build_dense_transpose(p->desc, &p->tptr, &p->tidx, &p->tw, &p->nnz, st);
+    if (e != cudaSuccess) return e;
+    p->desc.tptr = p->tptr;
+    p->desc.tidx = p->tidx;
+    p->desc.tw = p->tw;
+    return cudaSuccess;
+}
+
 static int warp_finish(mct_warp_plan* p, mct_warp_plan** out) {
     cudaError_t e = cudaMalloc(&p->d_desc, sizeof(WarpDesc));
     if (e == cudaSuccess) e = cudaMemcpy(p->d_desc, &p->desc, sizeof(WarpDesc), cudaMemcpyHostToDevice);
@@ -368,6 +380,11 @@ int mct_warp_plan_create_rigid(mct_warp_plan** plan, int rows, int cols, double 
     d.ext0 = fabs(cos_r) + fabs(sin_r);
     d.ext1 = d.ext0;
     p->desc = d;
+    cudaError_t e = attach_transpose(p, 0);
+    if (e != cudaSuccess) {
+        delete p;
+        return cuda_fail(e, "mct_warp_plan_create_rigid");
+    }
     return warp_finish(p, plan);
 }
 
@@ -385,6 +402,11 @@ int mct_warp_plan_create_dilatation(mct_warp_plan** plan, int rows, int cols, do
     d.ext0 = scale;
     d.ext1 = scale;
     p->desc = d;
+    cudaError_t e = attach_transpose(p, 0);
+    if (e != cudaSuccess) {
+        delete p;
+        return cuda_fail(e, "mct_warp_plan_create_dilatation");
+    }
     return warp_finish(p, plan);
 }
 

@@ -88,35 +88,15 @@ __device__ __forceinline__ float warp_apply_at(const WarpDesc& w, int r, int c, 
 }
 
 // Transpose at pixel q = (qr, qc): sum over output pixels p with q among taps(p)
-// of w(p, q) * y[p], reading y through `fetch(flat_index)`.  Deterministic
-// gather (fixed candidate order).
+// of w(p, q) * y[p], reading y through `fetch(flat_index)`.  The plan's
+// transposed gather list (sorted by p, built from warp_taps itself) makes the
+// weights bit-identical to the forward's and the order fixed (deterministic).
 template <typename Fetch>
 __device__ __forceinline__ float warp_adjoint_at(const WarpDesc& w, Fetch fetch, int qr, int qc) {
-    if (w.kind == MCT_WARP_IDENTITY) return fetch((long long)qr * w.cols + qc);
-    if (w.kind == MCT_WARP_DENSE) {
-        const long long q = (long long)qr * w.cols + qc;
-        int e0 = __ldg(w.tptr + q), e1 = __ldg(w.tptr + q + 1);
-        float acc = 0.0f;
-        for (int e = e0; e < e1; ++e) acc = fmaf(__ldg(w.tw + e), fetch(__ldg(w.tidx + e)), acc);
-        return acc;
-    }
-    // affine: candidates p in the bounding box of T([q-1, q+1]^2)
-    double uq = (double)qr - w.hr, vq = (double)qc - w.hc;
-    double cu = w.i00 * uq + w.i01 * vq + w.o0 + w.hr;
-    double cv = w.i10 * uq + w.i11 * vq + w.o1 + w.hc;
-    int rlo = max(0, (int)floor(fmax(cu - w.ext0, -2.0)) - 1);
-    int rhi = min(w.rows - 1, (int)ceil(fmin(cu + w.ext0, (double)w.rows + 2.0)) + 1);
-    int clo = max(0, (int)floor(fmax(cv - w.ext1, -2.0)) - 1);
-    int chi = min(w.cols - 1, (int)ceil(fmin(cv + w.ext1, (double)w.cols + 2.0)) + 1);
+    const long long q = (long long)qr * w.cols + qc;
+    if (w.kind == MCT_WARP_IDENTITY) return fetch(q);
+    const int e0 = __ldg(w.tptr + q), e1 = __ldg(w.tptr + q + 1);
     float acc = 0.0f;
-    for (int pr = rlo; pr <= rhi; ++pr) {
-        for (int pc = clo; pc <= chi; ++pc) {
-            TapSet t = warp_taps(w, pr, pc);
-            int dr = qr - t.r0, dc = qc - t.c0;
-            if ((unsigned)dr <= 1u && (unsigned)dc <= 1u) {
-                acc = fmaf(tap_weight(t, dr, dc), fetch((long long)pr * w.cols + pc), acc);
-            }
-        }
-    }
+    for (int e = e0; e < e1; ++e) acc = fmaf(__ldg(w.tw + e), fetch(__ldg(w.tidx + e)), acc);
     return acc;
 }
