@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--kernel-pass", type=int, default=3,
                     help="eager epochs instrumented per kernel for the roofline")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the torch.distributed gate-sharded path even for one rank "
+                         "(exercises the NCCL code path on a single GPU)")
     return ap.parse_args()
 
 
@@ -260,8 +263,12 @@ def run_ours(args, cfg):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    use_dist = world > 1 or args.force_dist
+    if use_dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
     m.build_native()
     problem, norms, stacked = build_problem(cfg, torch)
     pcfg = m.default_config("pdhg", norms, cfg.alpha, args.steps, stacked_norm_sq=stacked)
@@ -269,19 +276,19 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream()
 
     def barrier():
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(v):
-        if world == 1:
+        if not use_dist:
             return v
         t = torch.tensor([v], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     # ---------------- PDHG (gate-sharded across ranks) -------------------
-    if world == 1:
+    if not use_dist:
         eng = Engine([problem.operators], [problem.data])
         eng.set_params(pcfg)
         eng.reset()
@@ -325,7 +332,7 @@ def run_ours(args, cfg):
     items = eng.items_pdhg(epoch_ctr=True)
     ip, sp = ctypes.byref(items), ctypes.byref(eng._st)
     fam, ws, st = eng.family.handle, _lib.ptr(eng.ws), _lib.stream_handle()
-    dzp = _lib.ptr(worker.dz) if world > 1 else None
+    dzp = _lib.ptr(worker.dz) if use_dist else None
     calls = [
         ("K1_prox_warp", lambda: _lib.check(L.mct_iter_prox_warp(fam, ip, sp, eng.tau,
                                                                  problem.alpha, ws, st))),
@@ -420,7 +427,7 @@ def run_ours(args, cfg):
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
     return 0
