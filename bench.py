@@ -236,8 +236,7 @@ def build_problem(cfg, torch):
     from paper_2410_10503_b200 import workloads
 
     problem, truth, inp = m.simulate.workload_problem(cfg, 0)
-    # step sizes from the admissibility rule with analytic norm bounds is not
-    # the reference's rule; use device power iteration
+    # step sizes: device power iterations feed the reference's default_config rule
     norms = [m.power_method(op, iterations=20, seed=0) for op in problem.operators]
     stacked = m.stacked_norm_sq(problem.operators, iterations=20, seed=0)
     return problem, norms, stacked

@@ -182,7 +182,6 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     std::vector<AdjAngle> adj(num_angles);
     const double hr = 0.5 * (rows - 1), hc = 0.5 * (cols - 1);
     double hmax = 0.0;
-    p->has_rows = p->has_cols = 0;
     for (int a = 0; a < num_angles; ++a) {
         const double c = cos_a[a], s = sin_a[a];
         RayAngle& r = fwd[a];
@@ -198,7 +197,6 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
             r.Q = hc - hr * r.slope;
             m = fabs(c);
             r.cols_dom = 0;
-            p->has_rows = 1;
         } else {
             if (!(s > 0.0)) {
                 delete p;
@@ -210,7 +208,6 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
             r.Q = hr - hc * r.slope;
             m = s;
             r.cols_dom = 1;
-            p->has_cols = 1;
         }
         r.step = (float)(1.0 / m);
         r.slope_fx = llrint(r.slope * 4294967296.0);
@@ -370,15 +367,6 @@ int mct_warp_plan_create_rigid(mct_warp_plan** plan, int rows, int cols, double 
     d.sn = sin_r;
     d.tr = t_row;
     d.tc = t_col;
-    // inverse: p = R(theta) s + t  (motion.py:111-120 forward map T)
-    d.i00 = cos_r;
-    d.i01 = -sin_r;
-    d.i10 = sin_r;
-    d.i11 = cos_r;
-    d.o0 = t_row;
-    d.o1 = t_col;
-    d.ext0 = fabs(cos_r) + fabs(sin_r);
-    d.ext1 = d.ext0;
     p->desc = d;
     cudaError_t e = attach_transpose(p, 0);
     if (e != cudaSuccess) {
@@ -397,10 +385,6 @@ int mct_warp_plan_create_dilatation(mct_warp_plan** plan, int rows, int cols, do
     WarpDesc d = identity_desc(rows, cols);
     d.kind = MCT_WARP_DILATATION;
     d.scale = scale;
-    d.i00 = scale;
-    d.i11 = scale;
-    d.ext0 = scale;
-    d.ext1 = scale;
     p->desc = d;
     cudaError_t e = attach_transpose(p, 0);
     if (e != cudaSuccess) {

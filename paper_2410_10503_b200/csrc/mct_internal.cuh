@@ -49,7 +49,6 @@ struct mct_ray_plan {
     int wx, wxt;         // padded strides (floats)
     int pb, wy;          // sinogram pad (bins) and padded stride
     int kfoot;           // extra footprint bins for the adjoint (0 when sp >= step^-1)
-    int has_rows, has_cols;
     RayAngle* d_fwd;
     AdjAngle* d_adj;
     size_t off_x, off_xt, off_dy, off_img, img_slot_bytes, off_part, off_cnt, item_bytes;
@@ -72,10 +71,8 @@ struct WarpDesc {
     double hr, hc;           // (rows-1)/2, (cols-1)/2
     double cs, sn, tr, tc;   // rigid
     double scale;            // dilatation
-    // inverse map for the adjoint window: p = Minv * s + off (centred coords)
-    double i00, i01, i10, i11, o0, o1, ext0, ext1;
     const float* phi;        // dense (2, rows, cols)
-    const int* tptr;         // dense transposed gather list (rows*cols + 1)
+    const int* tptr;         // transposed gather list of D (rows*cols + 1), all non-identity kinds
     const int* tidx;
     const float* tw;
 };
