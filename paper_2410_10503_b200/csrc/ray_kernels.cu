@@ -133,9 +133,12 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
 }
 
 #define FWD_ANGLES MCT_FWD_ANGLES  // warps (= consecutive angles) per block; they share L1 lines
+#ifndef FWD_MIN_BLOCKS
+#define FWD_MIN_BLOCKS 12         // 12 x 4 warps resident: 40 registers for 8 loads in flight
+#endif
 
 template <int MODE>
-__global__ void __launch_bounds__(32 * FWD_ANGLES, 64 / FWD_ANGLES) fwd_kernel(FwdArgs p) {
+__global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(FwdArgs p) {
     const int ks = p.ksplit;
     const int item = blockIdx.z / ks;
     const int part = blockIdx.z - item * ks;
@@ -210,28 +213,33 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, 64 / FWD_ANGLES) fwd_kernel(F
             float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // sum of v0
             float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;  // sum of frac*2^24*(v1 - v0)
             int kk = kc;
-            for (; kk + 3 <= kend; kk += 4) {
-                unsigned l1 = flo, h1 = fhi;
-                fx_add(l1, h1, ilo, ihi);
-                unsigned l2 = l1, h2 = h1;
-                fx_add(l2, h2, ilo, ihi);
-                unsigned l3 = l2, h3 = h2;
-                fx_add(l3, h3, ilo, ihi);
-                const float2 v0 = __ldg(X2 + fhi);
-                const float2 v1 = __ldg(X2 + h1);
-                const float2 v2 = __ldg(X2 + h2);
-                const float2 v3 = __ldg(X2 + h3);
-                s0 += v0.x;
-                s1 += v1.x;
-                s2 += v2.x;
-                s3 += v3.x;
-                t0 = fmaf((float)(flo >> 8), v0.y - v0.x, t0);
-                t1 = fmaf((float)(l1 >> 8), v1.y - v1.x, t1);
-                t2 = fmaf((float)(l2 >> 8), v2.y - v2.x, t2);
-                t3 = fmaf((float)(l3 >> 8), v3.y - v3.x, t3);
-                flo = l3;
-                fhi = h3;
+            // 8 samples per trip: all 8 loads are issued before the first use
+            for (; kk + 7 <= kend; kk += 8) {
+                unsigned lo8[8], hi8[8];
+                lo8[0] = flo;
+                hi8[0] = fhi;
+#pragma unroll
+                for (int u = 1; u < 8; ++u) {
+                    lo8[u] = lo8[u - 1];
+                    hi8[u] = hi8[u - 1];
+                    fx_add(lo8[u], hi8[u], ilo, ihi);
+                }
+                float2 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldg(X2 + hi8[u]);
+                flo = lo8[7];
+                fhi = hi8[7];
                 fx_add(flo, fhi, ilo, ihi);
+                s0 += v[0].x; s1 += v[1].x; s2 += v[2].x; s3 += v[3].x;
+                t0 = fmaf((float)(lo8[0] >> 8), v[0].y - v[0].x, t0);
+                t1 = fmaf((float)(lo8[1] >> 8), v[1].y - v[1].x, t1);
+                t2 = fmaf((float)(lo8[2] >> 8), v[2].y - v[2].x, t2);
+                t3 = fmaf((float)(lo8[3] >> 8), v[3].y - v[3].x, t3);
+                s0 += v[4].x; s1 += v[5].x; s2 += v[6].x; s3 += v[7].x;
+                t0 = fmaf((float)(lo8[4] >> 8), v[4].y - v[4].x, t0);
+                t1 = fmaf((float)(lo8[5] >> 8), v[5].y - v[5].x, t1);
+                t2 = fmaf((float)(lo8[6] >> 8), v[6].y - v[6].x, t2);
+                t3 = fmaf((float)(lo8[7] >> 8), v[7].y - v[7].x, t3);
             }
             for (; kk <= kend; ++kk) {
                 const float2 v0 = __ldg(X2 + fhi);
