@@ -314,128 +314,200 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(Fw
 // angle a receives  step * max(0, 1 - |j - jc|*g) * dy[a, j]  from the bins j
 // around its detector coordinate jc = (v cos - u sin)/sp + (B-1)/2: exactly the
 // Joseph weight of projector.py:161-166 seen from the pixel (the tent identity
-// pinned by test_projector.py:78-93).
+// pinned by test_projector.py:78-93).  The sinogram is pre-scaled by the step.
 // jc is carried in 32.32 fixed point: an fp64 anchor per (tile, angle) plus
 // exact integer steps cos/sp, sin/sp per column / row, so the bin index and the
 // interpolation fraction are exact to ~1e-9 bins at any image size.
-// Each thread owns 8 consecutive rows of one column: the two shared-memory
-// broadcasts of the per-angle constants are amortised over 8 pixels, and a warp
-// reads one contiguous run of a sinogram row per pixel row (coalesced, L1); the
-// two bins of a pixel come from one pair-packed 8-byte load.
-// The angle loop may be split over blockIdx.z (partial image slots, summed in a
-// fixed order by K4).  fp32 partial sums per chunk of 128 angles, fp64 totals.
+//
+// Mirror pairing: angles theta_a and theta_{A-a} = pi - theta_a give the mirrored
+// pixel (u, -v) the same detector coordinate as (u, v).  A thread therefore owns
+// ADJ_PPT consecutive rows of a column c in the left half of the image *and* of
+// its mirror column cm = cols-1-c; for every angle pair (a, A-a) it computes two
+// sets of bin indices / tent weights (those of c and of cm at angle a) and uses
+// each twice: jc_a(c) = jc_{A-a}(cm) and jc_a(cm) = jc_{A-a}(c).  Half the
+// coordinate and weight arithmetic per pixel-angle; angles 0 and A/2
+// (self-paired) are done per pixel.
+// The angle pairs may be split over blockIdx.z (partial image slots, summed in
+// a fixed order by K4).  fp32 partial sums per chunk, fp64 totals.
 // ---------------------------------------------------------------------------
-#define ADJ_TW 32      // tile width (columns) = one warp
-#define ADJ_TH 32      // tile height (rows)
-#define ADJ_PPT 8      // consecutive rows per thread
-#define ADJ_THREADS (ADJ_TW * ADJ_TH / ADJ_PPT)
+#define ADJ_TW 32      // tile width (left-half columns) = one warp
+#define ADJ_PPT 4      // consecutive rows per thread
+#define ADJ_WARPS 4
+#define ADJ_TH (ADJ_PPT * ADJ_WARPS)
+#define ADJ_THREADS (ADJ_TW * ADJ_WARPS)
 #define ADJ_CH ADJ_THREADS
+#ifndef ADJ_MIN_BLOCKS
+#define ADJ_MIN_BLOCKS 10
+#endif
 #define INV_2_32 2.3283064365386963e-10f
 
-template <int K, bool FULL>
-__device__ __forceinline__ void adj_angle(const float2* __restrict__ DY2, unsigned tlo,
-                                          unsigned thi, unsigned slo, unsigned shi, float g32,
-                                          float omg, int nrows, float (&acc)[ADJ_PPT]) {
+// Tent weights of bins floor(jc) .. for a pixel whose jc has fraction tlo/2^32,
+// applied to two sinogram rows (pixel and mirror pixel).
+// One tent (bin index thi, fraction tlo/2^32) applied to two sinogram rows: row
+// thi's (pixel p at angle a) and row thi + delta's (the mirror of p at A-a).
+template <int K>
+__device__ __forceinline__ void adj_tap2(const float2* __restrict__ DY2, unsigned tlo, int thi,
+                                         int delta, float g32, float omg, float& acc_a,
+                                         float& acc_b) {
+    const float F = (float)tlo;
+    if (K == 0) {
+        const float2 v = __ldg(DY2 + (unsigned)thi);
+        const float2 vm = __ldg(DY2 + (unsigned)(thi + delta));
+        const float w0 = __saturatef(fmaf(-F, g32, 1.0f));  // bin floor(jc)
+        const float w1 = __saturatef(fmaf(F, g32, omg));    // bin floor(jc) + 1
+        acc_a = fmaf(w0, v.x, fmaf(w1, v.y, acc_a));
+        acc_b = fmaf(w0, vm.x, fmaf(w1, vm.y, acc_b));
+    } else {
+        const float d = F * INV_2_32;
+        const float g = g32 * 4294967296.0f;
 #pragma unroll
-    for (int m = 0; m < ADJ_PPT; ++m) {
-        if (FULL || m < nrows) {
-            // thi = sinogram row base + floor(jc) (>= 0), tlo = frac(jc) * 2^32; the
-            // sinogram is pre-scaled by the step, so only the tent weights remain
-            const float F = (float)tlo;
-            if (K == 0) {
-                const float2 v = __ldg(DY2 + thi);
-                const float w0 = __saturatef(fmaf(-F, g32, 1.0f));  // bin floor(jc)
-                const float w1 = __saturatef(fmaf(F, g32, omg));    // bin floor(jc) + 1
-                acc[m] = fmaf(w0, v.x, fmaf(w1, v.y, acc[m]));
-            } else {
-                const float d = F * INV_2_32;
-                const float g = g32 * 4294967296.0f;
-#pragma unroll
-                for (int mm = -K; mm <= K; mm += 2) {
-                    const float2 v = __ldg(DY2 + (int)thi + mm);
-                    const float wa = __saturatef(fmaf(-fabsf((float)mm - d), g, 1.0f));
-                    const float wb = __saturatef(fmaf(-fabsf((float)(mm + 1) - d), g, 1.0f));
-                    acc[m] = fmaf(wa, v.x, fmaf(wb, v.y, acc[m]));
-                }
-            }
+        for (int mm = -K; mm <= K; mm += 2) {
+            const float2 v = __ldg(DY2 + (thi + mm));
+            const float2 vm = __ldg(DY2 + (thi + delta + mm));
+            const float wa = __saturatef(fmaf(-fabsf((float)mm - d), g, 1.0f));
+            const float wb = __saturatef(fmaf(-fabsf((float)(mm + 1) - d), g, 1.0f));
+            acc_a = fmaf(wa, v.x, fmaf(wb, v.y, acc_a));
+            acc_b = fmaf(wa, vm.x, fmaf(wb, vm.y, acc_b));
         }
-        fx_sub(tlo, thi, slo, shi);
     }
 }
 
 template <int K>
-__global__ void __launch_bounds__(ADJ_THREADS, 12) adj_kernel(AdjArgs p) {
-    __shared__ longlong2 s_t[ADJ_CH];  // anchor (with sinogram row base), cos/sp
+__device__ __forceinline__ void adj_tap1(const float2* __restrict__ DY2, unsigned tlo, int thi,
+                                         float g32, float omg, float& acc) {
+    const float F = (float)tlo;
+    if (K == 0) {
+        const float2 v = __ldg(DY2 + (unsigned)thi);
+        const float w0 = __saturatef(fmaf(-F, g32, 1.0f));
+        const float w1 = __saturatef(fmaf(F, g32, omg));
+        acc = fmaf(w0, v.x, fmaf(w1, v.y, acc));
+    } else {
+        const float d = F * INV_2_32;
+        const float g = g32 * 4294967296.0f;
+#pragma unroll
+        for (int mm = -K; mm <= K; mm += 2) {
+            const float2 v = __ldg(DY2 + (thi + mm));
+            const float wa = __saturatef(fmaf(-fabsf((float)mm - d), g, 1.0f));
+            const float wb = __saturatef(fmaf(-fabsf((float)(mm + 1) - d), g, 1.0f));
+            acc = fmaf(wa, v.x, fmaf(wb, v.y, acc));
+        }
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(ADJ_THREADS, ADJ_MIN_BLOCKS) adj_kernel(AdjArgs p) {
+    __shared__ longlong2 s_t[ADJ_CH];  // anchor (with sinogram row base of a), cos/sp
     __shared__ int4 s_u[ADJ_CH];       // sin/sp (lo, hi), g*2^-32, 1 - g
+    __shared__ int s_d[ADJ_CH];        // sinogram offset of row A-a relative to row a
+    __shared__ double s_tot[2 * ADJ_PPT][ADJ_THREADS];
     const int item = blockIdx.z / p.asplit;
     const int split = blockIdx.z - item * p.asplit;
-    const int a_beg = (int)((long long)p.A * split / p.asplit);
-    const int a_end = (int)((long long)p.A * (split + 1) / p.asplit);
+    const int A = p.A;
+    const int npairs = (A - 1) / 2;  // pairs (a, A-a), a = 1 .. npairs
+    const int q_beg = 1 + (int)((long long)npairs * split / p.asplit);
+    const int q_end = 1 + (int)((long long)npairs * (split + 1) / p.asplit);
     const int tid = threadIdx.y * ADJ_TW + threadIdx.x;
+    const int ncl = (p.cols + 1) >> 1;                      // left-half columns (incl. centre)
     const int r0 = blockIdx.y * ADJ_TH, c0 = blockIdx.x * ADJ_TW;
-    const int c = c0 + threadIdx.x;
+    const int c = c0 + threadIdx.x;                          // primary column
+    const int cm = p.cols - 1 - c;                           // mirror column
     const int rt = r0 + threadIdx.y * ADJ_PPT;
-    const int nrows = min(ADJ_PPT, p.rows - rt);              // warp-uniform
-    const int txc = min((int)threadIdx.x, p.cols - 1 - c0);   // clamp lanes past the image
+    const int nrows = min(ADJ_PPT, p.rows - rt);             // warp-uniform
+    const int txc = min((int)threadIdx.x, ncl - 1 - c0);     // clamp lanes past the half
+    const int cmc = p.cols - 1 - (c0 + txc);                 // (clamped) mirror column
     const double u0 = (double)r0 - 0.5 * (double)(p.rows - 1);
     const double v0 = (double)c0 - 0.5 * (double)(p.cols - 1);
     const char* base = p.ws + (size_t)item * p.item_bytes;
     const float2* __restrict__ DY2 = reinterpret_cast<const float2*>(base + p.off_dy);
     const long long row_off = (long long)(threadIdx.y * ADJ_PPT);
 
-    // fp64 running totals live in shared memory (flushed once per 128-angle
-    // chunk) so the registers go to the in-flight loads
-    __shared__ double s_tot[ADJ_PPT][ADJ_THREADS];
 #pragma unroll
-    for (int m = 0; m < ADJ_PPT; ++m) s_tot[m][tid] = 0.0;
-    for (int a0 = a_beg; a0 < a_end; a0 += ADJ_CH) {
-        const int cnt = min(ADJ_CH, a_end - a0);
+    for (int m = 0; m < 2 * ADJ_PPT; ++m) s_tot[m][tid] = 0.0;
+
+    // ---- self-paired angles 0 and A/2 (split 0 only), pixel by pixel
+    if (split == 0) {
+        const int nsingle = (A % 2 == 0 && A >= 2) ? 2 : 1;
+        for (int si = 0; si < nsingle; ++si) {
+            const int a = si == 0 ? 0 : A / 2;
+            const AdjAngle aa = p.ang[a];
+            const double jcA = v0 * aa.cs - u0 * aa.sn + p.jmid;
+            const long long TA =
+                __double2ll_rn(jcA * FX_ONE) + ((long long)(a * p.wy + p.pb) << 32);
+            const float g32 = aa.g * INV_2_32, omg = 1.0f - aa.g;
+            long long T = TA + (long long)txc * aa.csx - row_off * aa.snx;
+            long long Tm = TA + (long long)(cmc - c0) * aa.csx - row_off * aa.snx;
+            for (int m = 0; m < nrows; ++m) {
+                float acc = 0.0f, accm = 0.0f;
+                adj_tap1<K>(DY2, (unsigned)T, (int)(T >> 32), g32, omg, acc);
+                adj_tap1<K>(DY2, (unsigned)Tm, (int)(Tm >> 32), g32, omg, accm);
+                s_tot[m][tid] += (double)acc;
+                s_tot[ADJ_PPT + m][tid] += (double)accm;
+                T -= aa.snx;
+                Tm -= aa.snx;
+            }
+        }
+    }
+
+    // ---- mirror pairs (a, A-a)
+    for (int q0 = q_beg; q0 < q_end; q0 += ADJ_CH) {
+        const int cnt = min(ADJ_CH, q_end - q0);
         __syncthreads();
         if (tid < cnt) {
-            const AdjAngle aa = p.ang[a0 + tid];
+            const int a = q0 + tid;
+            const AdjAngle aa = p.ang[a];
             const double jcA = v0 * aa.cs - u0 * aa.sn + p.jmid;
-            const long long TA = __double2ll_rn(jcA * FX_ONE) +
-                                 ((long long)((a0 + tid) * p.wy + p.pb) << 32);
+            const long long TA =
+                __double2ll_rn(jcA * FX_ONE) + ((long long)(a * p.wy + p.pb) << 32);
             s_t[tid] = make_longlong2(TA, aa.csx);
             s_u[tid] = make_int4((int)(unsigned)aa.snx, (int)(aa.snx >> 32),
                                  __float_as_int(aa.g * INV_2_32), __float_as_int(1.0f - aa.g));
+            s_d[tid] = (A - 2 * a) * p.wy;
         }
         __syncthreads();
         if (nrows <= 0) continue;
-        float acc[ADJ_PPT];
+        float acc[ADJ_PPT], accm[ADJ_PPT];
 #pragma unroll
-        for (int m = 0; m < ADJ_PPT; ++m) acc[m] = 0.0f;
-        if (nrows == ADJ_PPT) {
+        for (int m = 0; m < ADJ_PPT; ++m) acc[m] = accm[m] = 0.0f;
 #pragma unroll 2
-            for (int t = 0; t < cnt; ++t) {
-                const longlong2 T2 = s_t[t];
-                const int4 U = s_u[t];
-                const long long snx = ((long long)U.y << 32) | (unsigned)U.x;
-                const float g32 = __int_as_float(U.z), omg = __int_as_float(U.w);
-                const long long T = T2.x + (long long)txc * T2.y - row_off * snx;
-                adj_angle<K, true>(DY2, (unsigned)T, (unsigned)(T >> 32), (unsigned)U.x,
-                                   (unsigned)U.y, g32, omg, nrows, acc);
-            }
-        } else {
-            for (int t = 0; t < cnt; ++t) {
-                const longlong2 T2 = s_t[t];
-                const int4 U = s_u[t];
-                const long long snx = ((long long)U.y << 32) | (unsigned)U.x;
-                const float g32 = __int_as_float(U.z), omg = __int_as_float(U.w);
-                const long long T = T2.x + (long long)txc * T2.y - row_off * snx;
-                adj_angle<K, false>(DY2, (unsigned)T, (unsigned)(T >> 32), (unsigned)U.x,
-                                    (unsigned)U.y, g32, omg, nrows, acc);
+        for (int t = 0; t < cnt; ++t) {
+            const longlong2 T2 = s_t[t];
+            const int4 U = s_u[t];
+            const int delta = s_d[t];
+            const long long snx = ((long long)U.y << 32) | (unsigned)U.x;
+            const float g32 = __int_as_float(U.z), omg = __int_as_float(U.w);
+            // c at angle a == cm at angle A-a ; cm at angle a == c at angle A-a
+            const long long T = T2.x + (long long)txc * T2.y - row_off * snx;
+            const long long Tm = T2.x + (long long)(cmc - c0) * T2.y - row_off * snx;
+            unsigned tlo = (unsigned)T, thi = (unsigned)(T >> 32);
+            unsigned mlo = (unsigned)Tm, mhi = (unsigned)(Tm >> 32);
+#pragma unroll
+            for (int m = 0; m < ADJ_PPT; ++m) {
+                if (m < nrows) {
+                    adj_tap2<K>(DY2, tlo, (int)thi, delta, g32, omg, acc[m], accm[m]);
+                    adj_tap2<K>(DY2, mlo, (int)mhi, delta, g32, omg, accm[m], acc[m]);
+                }
+                fx_sub(tlo, thi, (unsigned)U.x, (unsigned)U.y);
+                fx_sub(mlo, mhi, (unsigned)U.x, (unsigned)U.y);
             }
         }
 #pragma unroll
-        for (int m = 0; m < ADJ_PPT; ++m) s_tot[m][tid] += (double)acc[m];
+        for (int m = 0; m < ADJ_PPT; ++m) {
+            s_tot[m][tid] += (double)acc[m];
+            s_tot[ADJ_PPT + m][tid] += (double)accm[m];
+        }
     }
-    if (c >= p.cols) return;
+    if (c >= ncl) return;
     float* IMG = reinterpret_cast<float*>(const_cast<char*>(base) + p.off_img +
                                           (size_t)split * p.img_slot_bytes);
-#pragma unroll
-    for (int m = 0; m < ADJ_PPT; ++m)
-        if (m < nrows) IMG[(long long)(rt + m) * p.cols + c] = (float)s_tot[m][tid];
+    for (int m = 0; m < nrows; ++m) {
+        const long long row = (long long)(rt + m) * p.cols;
+        if (cm == c) {  // centre column of an odd width: the primary role already
+            IMG[row + c] = (float)s_tot[m][tid];  // holds every angle (mirror = duplicate)
+        } else {
+            IMG[row + c] = (float)s_tot[m][tid];
+            IMG[row + cm] = (float)s_tot[ADJ_PPT + m][tid];
+        }
+    }
 }
 
 }  // namespace
@@ -467,6 +539,8 @@ cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st) {
 // Angle split of A^*: fill one wave of resident blocks when a launch has few
 // tiles (single-gate SPDHG), never exceeding it (a partial second wave would
 // idle most SMs); every split keeps >= 16 angles.
+static inline int adj_tiles_x(int cols) { return ((cols + 1) / 2 + ADJ_TW - 1) / ADJ_TW; }
+
 int choose_asplit(const mct_ray_plan* rp, int items) {
     static int slots = 0;  // resident adj blocks per GPU (queried once)
     if (slots == 0) {
@@ -478,18 +552,18 @@ int choose_asplit(const mct_ray_plan* rp, int items) {
             per_sm = 8;
         slots = sms * per_sm;
     }
-    const long long tiles = (long long)((rp->cols + ADJ_TW - 1) / ADJ_TW) *
-                            ((rp->rows + ADJ_TH - 1) / ADJ_TH) * (items > 0 ? items : 1);
+    const long long tiles = (long long)adj_tiles_x(rp->cols) * ((rp->rows + ADJ_TH - 1) / ADJ_TH) *
+                            (items > 0 ? items : 1);
     long long s = tiles >= slots ? 1 : slots / tiles;
     s = s < 1 ? 1 : s;
     s = s > MCT_MAX_ASPLIT ? MCT_MAX_ASPLIT : s;
-    const long long by_angles = rp->A / 16 > 0 ? rp->A / 16 : 1;
+    const long long by_angles = rp->A / 32 > 0 ? rp->A / 32 : 1;  // >= 16 pairs per split
     return (int)(s < by_angles ? s : by_angles);
 }
 
 cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, cudaStream_t st) {
-    dim3 block(ADJ_TW, ADJ_TH / ADJ_PPT),
-        grid((a.cols + ADJ_TW - 1) / ADJ_TW, (a.rows + ADJ_TH - 1) / ADJ_TH, items * a.asplit);
+    dim3 block(ADJ_TW, ADJ_WARPS),
+        grid(adj_tiles_x(a.cols), (a.rows + ADJ_TH - 1) / ADJ_TH, items * a.asplit);
     switch (kfoot) {
         case 0: adj_kernel<0><<<grid, block, 0, st>>>(a); break;
         case 1: adj_kernel<1><<<grid, block, 0, st>>>(a); break;
