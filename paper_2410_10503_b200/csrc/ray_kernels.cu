@@ -12,12 +12,14 @@ namespace {
 
 // ---------------------------------------------------------------------------
 // K1 / pack: W = D_g(x_new), x_new = prox_g(x - tau*zbar) (or x_new = x), written
-// into the pair-packed padded row-major X2 and transposed XT2 of the item
-// workspace.  Tile 32x32, block 32x8, the transposed store staged through smem.
-// Pair packing: value W[r][c] is stored as X2[r][c].x and X2[r][c-1].y.
+// into the padded row-major X2 and transposed XT2 of the item workspace in the
+// "value + forward difference" pair layout: X2[r][c] = (W[r][c], W[r][c+1] -
+// W[r][c]) (zero outside the image), so a Joseph sample is one 8-byte load and
+// one FMA, v.x + frac * v.y.  A 32x32 tile plus a one-pixel halo of W is built
+// in shared memory, then both layouts are stored coalesced.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) pack_kernel(PackArgs p) {
-    __shared__ float tile[32][33];
+    __shared__ float tile[33][34];
     const int item = blockIdx.z;
     int slice, gate, iter;
     resolve_item(p.sel, item, slice, gate, iter);
@@ -43,46 +45,47 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs p) {
     };
 
     char* base = p.ws + (size_t)item * p.item_bytes;
-    float* X = reinterpret_cast<float*>(base + p.off_x) + 2 * MCT_PADX;
-    float* XT = reinterpret_cast<float*>(base + p.off_xt) + 2 * MCT_PADX;
+    float2* X = reinterpret_cast<float2*>(base + p.off_x) + MCT_PADX;
+    float2* XT = reinterpret_cast<float2*>(base + p.off_xt) + MCT_PADX;
 
     const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
-    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
     const bool writer = prox && k_in_slice == 0 && p.x_next != nullptr;
     bool bad = false;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        int r = r0 + ty + 8 * k, c = c0 + tx;
+    for (int idx = tid; idx < 33 * 33; idx += 256) {
+        const int i = idx / 33, jj = idx - i * 33;
+        const int r = r0 + i, c = c0 + jj;
         float w = 0.0f;
         if (r < rows && c < cols) {
-            if (ident) {
-                w = xnew(r, c);
-            } else {
-                w = warp_apply_at(wd, r, c, xnew);
-            }
-            const long long e = 2 * ((long long)r * p.wx + c);
-            X[e] = w;
-            X[e - 1] = w;
-            if (writer) {
-                float xn = xnew(r, c);
+            w = ident ? xnew(r, c) : warp_apply_at(wd, r, c, xnew);
+            if (writer && i < 32 && jj < 32) {
+                const float xn = xnew(r, c);
                 p.x_next[(long long)slice * p.x_slice_stride + (long long)r * cols + c] = xn;
                 bad |= !isfinite(xn);
             }
         }
-        tile[ty + 8 * k][tx] = w;
+        tile[i][jj] = w;
     }
     if (writer && p.status && __any_sync(0xffffffffu, bad)) {
         if ((threadIdx.x & 31) == 0) atomicMin(p.status, (unsigned long long)iter);
     }
     __syncthreads();
+    const int tx = threadIdx.x, ty = threadIdx.y;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        int c = c0 + ty + 8 * k, r = r0 + tx;
+        const int i = ty + 8 * k;
+        const int r = r0 + i, c = c0 + tx;
         if (r < rows && c < cols) {
-            const long long e = 2 * ((long long)c * p.wxt + r);
-            const float w = tile[tx][ty + 8 * k];
-            XT[e] = w;
-            XT[e - 1] = w;
+            const float w = tile[i][tx];
+            X[(long long)r * p.wx + c] = make_float2(w, tile[i][tx + 1] - w);
+            if (c == 0) X[(long long)r * p.wx - 1] = make_float2(0.0f, w);
+        }
+        // transposed: element (c, r) pairs W[r][c] with W[r+1][c]
+        const int ct = c0 + i, rt = r0 + tx;
+        if (rt < rows && ct < cols) {
+            const float w = tile[tx][i];
+            XT[(long long)ct * p.wxt + rt] = make_float2(w, tile[tx + 1][i] - w);
+            if (rt == 0) XT[(long long)ct * p.wxt - 1] = make_float2(0.0f, w);
         }
     }
 }
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(Fw
             const int i0 = (int)fhi - rowoff;
             if ((unsigned)(i0 + 1) < lim1) {
                 const float2 v = __ldg(X2 + fhi);
-                ea += fmaf((float)(flo >> 8) * INV_2_24, v.y - v.x, v.x);
+                ea += fmaf((float)(flo >> 8) * INV_2_24, v.y, v.x);
             }
             fx_add(flo, fhi, ilo, ihi);
             rowoff += stride;
@@ -211,7 +214,7 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(Fw
         for (int kc = k; kc <= chi; kc += 64) {
             const int kend = min(chi, kc + 63);
             float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // sum of v0
-            float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;  // sum of frac*2^24*(v1 - v0)
+            float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;  // sum of frac*2^24*(x[i+1] - x[i])
             int kk = kc;
             // 8 samples per trip: all 8 loads are issued before the first use
             for (; kk + 7 <= kend; kk += 8) {
@@ -231,20 +234,20 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(Fw
                 fhi = hi8[7];
                 fx_add(flo, fhi, ilo, ihi);
                 s0 += v[0].x; s1 += v[1].x; s2 += v[2].x; s3 += v[3].x;
-                t0 = fmaf((float)(lo8[0] >> 8), v[0].y - v[0].x, t0);
-                t1 = fmaf((float)(lo8[1] >> 8), v[1].y - v[1].x, t1);
-                t2 = fmaf((float)(lo8[2] >> 8), v[2].y - v[2].x, t2);
-                t3 = fmaf((float)(lo8[3] >> 8), v[3].y - v[3].x, t3);
+                t0 = fmaf((float)(lo8[0] >> 8), v[0].y, t0);
+                t1 = fmaf((float)(lo8[1] >> 8), v[1].y, t1);
+                t2 = fmaf((float)(lo8[2] >> 8), v[2].y, t2);
+                t3 = fmaf((float)(lo8[3] >> 8), v[3].y, t3);
                 s0 += v[4].x; s1 += v[5].x; s2 += v[6].x; s3 += v[7].x;
-                t0 = fmaf((float)(lo8[4] >> 8), v[4].y - v[4].x, t0);
-                t1 = fmaf((float)(lo8[5] >> 8), v[5].y - v[5].x, t1);
-                t2 = fmaf((float)(lo8[6] >> 8), v[6].y - v[6].x, t2);
-                t3 = fmaf((float)(lo8[7] >> 8), v[7].y - v[7].x, t3);
+                t0 = fmaf((float)(lo8[4] >> 8), v[4].y, t0);
+                t1 = fmaf((float)(lo8[5] >> 8), v[5].y, t1);
+                t2 = fmaf((float)(lo8[6] >> 8), v[6].y, t2);
+                t3 = fmaf((float)(lo8[7] >> 8), v[7].y, t3);
             }
             for (; kk <= kend; ++kk) {
                 const float2 v0 = __ldg(X2 + fhi);
                 s0 += v0.x;
-                t0 = fmaf((float)(flo >> 8), v0.y - v0.x, t0);
+                t0 = fmaf((float)(flo >> 8), v0.y, t0);
                 fx_add(flo, fhi, ilo, ihi);
             }
             dacc += (double)((s0 + s1) + (s2 + s3)) +
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(Fw
             const int i0 = (int)fhi - rowoff;
             if ((unsigned)(i0 + 1) < lim1) {
                 const float2 v = __ldg(X2 + fhi);
-                ea += fmaf((float)(flo >> 8) * INV_2_24, v.y - v.x, v.x);
+                ea += fmaf((float)(flo >> 8) * INV_2_24, v.y, v.x);
             }
             fx_add(flo, fhi, ilo, ihi);
             rowoff += stride;
