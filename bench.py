@@ -372,23 +372,55 @@ def run_ours(args, cfg):
     # ---------------- e2e through the C-ABI with host buffers ---------------
     e2e = None
     if not args.no_e2e:
+        # Every step streams that step's 20 gated sinograms host -> device (pinned)
+        # and reads x back.  The H2D of step k+1 runs on a copy stream into the
+        # second of two device data buffers while step k computes on the first.
         host_d = torch.from_numpy(np.stack([np.asarray(d, dtype=np.float32)
                                             for d in problem.data])[None]).pin_memory()
         host_x = torch.empty(eng.x.shape, dtype=torch.float32).pin_memory()
+        d_bufs = [eng.d, torch.empty_like(eng.d)]
+        runners = []
+        for b in range(2):
+            eng.set_data_buffer(d_bufs[b])
+            if not use_dist:
+                runners.append(eng.epoch_graph("pdhg", problem.alpha).replay)
+            else:
+                runners.append(step_fn)
+        eng.set_data_buffer(d_bufs[0])
+        copy_s = torch.cuda.Stream()
+        ev_done = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_copied = [torch.cuda.Event(), torch.cuda.Event()]
 
-        def e2e_step():
-            eng.d.copy_(host_d, non_blocking=True)
-            step_fn()
-            host_x.copy_(eng.x, non_blocking=True)
+        def e2e_run(K):
+            with torch.cuda.stream(copy_s):
+                copy_s.wait_stream(stream)
+                d_bufs[0].copy_(host_d, non_blocking=True)
+                ev_copied[0].record(copy_s)
+            for k in range(K):
+                b = k & 1
+                stream.wait_event(ev_copied[b])
+                if use_dist:
+                    eng.set_data_buffer(d_bufs[b])
+                runners[b]()
+                ev_done[b].record(stream)
+                host_x.copy_(eng.x, non_blocking=True)   # the step's result, D2H
+                if k + 1 < K:
+                    nb = 1 - b
+                    with torch.cuda.stream(copy_s):
+                        if k >= 1:
+                            copy_s.wait_event(ev_done[nb])  # step k-1 has read buffer nb
+                        d_bufs[nb].copy_(host_d, non_blocking=True)
+                        ev_copied[nb].record(copy_s)
+            stream.wait_stream(copy_s)
 
-        for _ in range(2):
-            e2e_step()
+        e2e_run(2)
         barrier()
-        e_ms = max_over_ranks(event_time(torch, lambda: [e2e_step() for _ in range(args.steps)],
-                                         stream)) / args.steps
+        e_ms = max_over_ranks(event_time(torch, lambda: e2e_run(args.steps), stream)) / args.steps
+        eng.set_data_buffer(d_bufs[0])
         e2e = {"value": 1000.0 / e_ms, "unit": "epochs/s",
                "h2d_bytes_per_step": int(host_d.numel() * 4),
-               "d2h_bytes_per_step": int(host_x.numel() * 4)}
+               "d2h_bytes_per_step": int(host_x.numel() * 4),
+               "overlap": "H2D of step k+1 (copy stream, double-buffered) overlaps step k"}
 
     # ---------------- CPU baseline (rank 0, N=1) ----------------------------
     cpu = None

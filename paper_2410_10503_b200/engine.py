@@ -247,9 +247,18 @@ class Engine:
                 self.iteration(self.items_spdhg(k), alpha)
         self.advance_epoch()
 
+    def set_data_buffer(self, d):
+        """Point the kernels at another (S, N, A, B) fp32 data buffer (double-buffered
+        streaming of new sinograms while an epoch computes)."""
+        if tuple(d.shape) != tuple(self.d.shape) or d.dtype != self.d.dtype or not d.is_cuda:
+            raise ValueError("data buffer must match the engine's (S, N, A, B) fp32 layout")
+        self.d = d
+        self._bind()
+
     def epoch_graph(self, mode: str, alpha: float):
-        """CUDA graph replaying one epoch (epoch counter advanced inside)."""
-        key = (mode, float(alpha), self.tau)
+        """CUDA graph replaying one epoch (epoch counter advanced inside); one graph per
+        (mode, alpha, tau, data buffer)."""
+        key = (mode, float(alpha), self.tau, self.d.data_ptr())
         g = self.graphs.get(key)
         if g is None:
             torch = self.torch
