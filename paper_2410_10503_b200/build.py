@@ -60,7 +60,8 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
         return LIB_PATH
     NATIVE_DIR.mkdir(parents=True, exist_ok=True)
     tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [_nvcc(), *ARCH_FLAGS, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(tmp)]
+    extra = os.environ.get("MCT_NVCC_EXTRA", "").split()  # tuning experiments only
+    cmd = [_nvcc(), *ARCH_FLAGS, *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-o", str(tmp)]
     cmd += [str(s) for s in sources()]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     log = NATIVE_DIR / "build.log"

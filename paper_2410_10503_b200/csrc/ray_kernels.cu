@@ -334,8 +334,12 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(Fw
 // a fixed order by K4).  fp32 partial sums per chunk, fp64 totals.
 // ---------------------------------------------------------------------------
 #define ADJ_TW 32      // tile width (left-half columns) = one warp
+#ifndef ADJ_PPT
 #define ADJ_PPT 4      // consecutive rows per thread
+#endif
+#ifndef ADJ_WARPS
 #define ADJ_WARPS 4
+#endif
 #define ADJ_TH (ADJ_PPT * ADJ_WARPS)
 #define ADJ_THREADS (ADJ_TW * ADJ_WARPS)
 #define ADJ_CH ADJ_THREADS
