@@ -49,8 +49,6 @@ def parse():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--kernel-pass", type=int, default=3,
-                    help="eager epochs instrumented per kernel for the roofline")
     ap.add_argument("--force-dist", action="store_true",
                     help="use the torch.distributed gate-sharded path even for one rank "
                          "(exercises the NCCL code path on a single GPU)")
@@ -287,32 +285,57 @@ def run_ours(args, cfg):
         return float(t.item())
 
     # ---------------- PDHG (gate-sharded across ranks) -------------------
+    # The timed region launches the four fused kernels of every epoch eagerly
+    # with a CUDA event between consecutive kernels on the launching stream, so
+    # the per-kernel durations used by the roofline come from the timed region
+    # itself (at C3 the GPU runs ~3 ms behind the host: launches never starve it).
+    import ctypes
+
+    L = _lib.load()
     if not use_dist:
         eng = Engine([problem.operators], [problem.data])
-        eng.set_params(pcfg)
-        eng.reset()
-        graph = eng.epoch_graph("pdhg", problem.alpha)
-        step_fn = graph.replay
-        launches_per_step = 5
+        worker = None
     else:
         worker = ShardedPDHG(pcfg, problem, rank, world)
         eng = worker.engine
+    eng.set_params(pcfg)
+    eng.reset()
+    items = eng.items_pdhg(epoch_ctr=True)
+    ip, sp = ctypes.byref(items), ctypes.byref(eng._st)
+    fam, ws, st = eng.family.handle, _lib.ptr(eng.ws), _lib.stream_handle(stream)
+    dzp = _lib.ptr(worker.dz) if use_dist else None
+    names = ["K1_prox_warp", "K2_forward_dual", "K3_adjoint", "K4_adjoint_update"]
+    calls = [
+        lambda: _lib.check(L.mct_iter_prox_warp(fam, ip, sp, eng.tau, problem.alpha, ws, st)),
+        lambda: _lib.check(L.mct_iter_forward_dual(fam, ip, sp, ws, st)),
+        lambda: _lib.check(L.mct_iter_adjoint(fam, ip, ws, st)),
+        lambda: _lib.check(L.mct_iter_adjoint_update(fam, ip, sp, dzp, ws, st)),
+    ]
 
-        def step_fn():
-            dz = worker.local_iteration()
-            dist.all_reduce(dz, op=dist.ReduceOp.SUM)
-            worker.finish(dz)
+    def step_fn(evs=None):
+        for i, call in enumerate(calls):
+            if evs is not None:
+                evs[i].record(stream)
+            call()
+        if evs is not None:
+            evs[4].record(stream)
+        if use_dist:
+            dist.all_reduce(worker.dz, op=dist.ReduceOp.SUM)
+            eng.z_update(worker.dz, pcfg.theta)
+        eng.advance_epoch()
 
-        launches_per_step = 6
+    launches_per_step = 6 if use_dist else 5
     for _ in range(args.warmup):
         step_fn()
     hbm_peak, peak_src = peaks()
+    step_events = [[torch.cuda.Event(enable_timing=True) for _ in range(5)]
+                   for _ in range(args.steps)]
     barrier()
     with ClockSampler(local) as clocks:
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record(stream)
-        for _ in range(args.steps):
-            step_fn()
+        for k in range(args.steps):
+            step_fn(step_events[k])
         end.record(stream)
         barrier()
     ms_total = max_over_ranks(start.elapsed_time(end))
@@ -322,27 +345,8 @@ def run_ours(args, cfg):
                           "primal": primal, "dual": dual}), file=sys.stderr)
     ms_step = ms_total / args.steps
     value = 1000.0 / ms_step
-
-    # ---------------- per-kernel timing pass (eager, events per launch) -----
-    L = _lib.load()
-    kern = {"K1_prox_warp": 0.0, "K2_forward_dual": 0.0, "K3_adjoint": 0.0, "K4_adjoint_update": 0.0}
-    import ctypes
-
-    items = eng.items_pdhg(epoch_ctr=True)
-    ip, sp = ctypes.byref(items), ctypes.byref(eng._st)
-    fam, ws, st = eng.family.handle, _lib.ptr(eng.ws), _lib.stream_handle()
-    dzp = _lib.ptr(worker.dz) if use_dist else None
-    calls = [
-        ("K1_prox_warp", lambda: _lib.check(L.mct_iter_prox_warp(fam, ip, sp, eng.tau,
-                                                                 problem.alpha, ws, st))),
-        ("K2_forward_dual", lambda: _lib.check(L.mct_iter_forward_dual(fam, ip, sp, ws, st))),
-        ("K3_adjoint", lambda: _lib.check(L.mct_iter_adjoint(fam, ip, ws, st))),
-        ("K4_adjoint_update", lambda: _lib.check(L.mct_iter_adjoint_update(fam, ip, sp, dzp, ws,
-                                                                           st))),
-    ]
-    for _ in range(args.kernel_pass):
-        for name, fn in calls:
-            kern[name] += event_time(torch, fn, stream) / args.kernel_pass
+    kern = {n: float(np.mean([ev[i].elapsed_time(ev[i + 1]) for ev in step_events]))
+            for i, n in enumerate(names)}
     items_per_launch = eng.local * eng.S
     ab = alg_bytes(cfg)
     iter_ms = sum(kern.values())
@@ -386,6 +390,9 @@ def run_ours(args, cfg):
                 runners.append(eng.epoch_graph("pdhg", problem.alpha).replay)
             else:
                 runners.append(step_fn)
+        eng.set_data_buffer(d_bufs[0])
+        if use_dist:
+            ip, sp = ctypes.byref(items), ctypes.byref(eng._st)  # re-bound state pointers
         eng.set_data_buffer(d_bufs[0])
         copy_s = torch.cuda.Stream()
         ev_done = [torch.cuda.Event(), torch.cuda.Event()]
