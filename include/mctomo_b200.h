@@ -229,6 +229,17 @@ int mct_axpby_mixed(long long n, double alpha, const void* x_dev, int x_is_f64, 
 int mct_dot_f64(const double* a_dev, const double* b_dev, long long n, double* out_dev,
                 double* scratch_dev, void* stream);
 
+/* ------------------------------------------------------------ data generation */
+/* Seeded Gaussian sinogram noise on the device, the documented recipe of
+ * simulate.gaussian_field (simulate.py:113-133) used by simulate.generate
+ * (simulate.py:191-239): numpy's Philox4x64-10 stream keyed
+ * (key0 = master_seed mod 2^64, key1 = gate_index), uniforms u1 then u2
+ * (ceil(count/2) each, bit-identical to numpy), Box-Muller pairs.
+ * out[i] = (base ? base[i] : 0) + scale * z_i in fp64 arithmetic, stored fp64
+ * (out_is_f64 = 1) or rounded to fp32.  count = 0 is a no-op.                 */
+int mct_gaussian_field(uint64_t key0, uint64_t key1, long long count, double scale,
+                       const float* base_dev, void* out_dev, int out_is_f64, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

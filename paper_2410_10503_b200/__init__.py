@@ -8,13 +8,17 @@ computed by hand-written sm_100a kernels behind a C-ABI
 """
 
 from .build import build_native
-from .experiment_io import ConvergenceRecord, rmse
+from .experiment_io import (ConvergenceRecord, RasterFormatError, RateFit, fit_rate,
+                            load_dataset, load_saddle, read_raster, rmse, save_dataset,
+                            save_saddle, write_raster)
 from .functionals import fit_value, g_value, moduli, prox_fstar, prox_g
 from .linops import (ComposedMap, GramSumMap, LinearMap, adjoint_mismatch, compose,
                      power_method, stacked_norm_sq)
 from .motion import DenseWarpOperator, MotionParams, WarpOperator, motion_sequence
 from .projector import Geometry, GatedOperator, RayTransform, adjoint, forward, ray_transform
-from .simulate import estimate_norms, gate_operators, gaussian_field, simulate_data
+from .simulate import (PHANTOM_KINDS, GatedDataset, NoiseModel, estimate_norms, gate_operators,
+                       gaussian_field, gaussian_field_device, generate, make_phantom,
+                       nonrigid_preset, rigid_preset, simulate_data)
 from .solvers import (RHO, DivergenceError, Problem, SaddlePoint, SolverConfig, SolverState,
                       cg_reference, default_config, draw_sequence, optimality_residual, run,
                       run_batch, sample_gates, step)

@@ -19,6 +19,7 @@ REDUCE_DOT, REDUCE_SQDIFF = 0, 1
 
 c_int, c_int32, c_double, c_void_p = ctypes.c_int, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 c_size_t, c_longlong, c_float = ctypes.c_size_t, ctypes.c_longlong, ctypes.c_float
+c_uint64 = ctypes.c_uint64
 PP = ctypes.POINTER(c_void_p)
 
 
@@ -94,6 +95,8 @@ SIGNATURES = {
     "mct_axpby_mixed": (c_int, [c_longlong, c_double, c_void_p, c_int, c_double, c_void_p, c_int,
                                 c_void_p]),
     "mct_dot_f64": (c_int, [c_void_p, c_void_p, c_longlong, c_void_p, c_void_p, c_void_p]),
+    "mct_gaussian_field": (c_int, [c_uint64, c_uint64, c_longlong, c_double, c_void_p, c_void_p,
+                                   c_int, c_void_p]),
 }
 
 _LIB = None

@@ -718,4 +718,16 @@ int mct_dot_f64(const double* a, const double* b, long long n, double* out, doub
     return MCT_OK;
 }
 
+// ------------------------------------------------------------ data generation
+int mct_gaussian_field(uint64_t key0, uint64_t key1, long long count, double scale,
+                       const float* base, void* out, int out_is_f64, void* stream) {
+    MCT_REQUIRE(count >= 0, "count must be >= 0");
+    MCT_REQUIRE(count == 0 || out, "null output");
+    MCT_REQUIRE(out_is_f64 == 0 || out_is_f64 == 1, "out_is_f64 must be 0 or 1");
+    MCT_CUDA(launch_gaussian_field(key0, key1, count, scale, base, out, out_is_f64,
+                                   (cudaStream_t)stream),
+             "gaussian field");
+    return MCT_OK;
+}
+
 }  // extern "C"

@@ -209,5 +209,9 @@ cudaError_t launch_absmax(const float* x, long long n, float* out, cudaStream_t 
 cudaError_t build_dense_transpose(const WarpDesc& desc, int** tptr, int** tidx, float** tw,
                                   long long* nnz, cudaStream_t st);
 
+cudaError_t launch_gaussian_field(unsigned long long k0, unsigned long long k1, long long count,
+                                  double scale, const float* base, void* out, int out_f64,
+                                  cudaStream_t st);
+
 // error reporting (abi.cu)
 int mct_set_error(int code, const std::string& msg);

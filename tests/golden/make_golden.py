@@ -188,10 +188,71 @@ def solver_c1():
     np.savez_compressed(HERE / "solver_c1.npz", **out)
 
 
+def dataset_cases():
+    """Data generation + file formats (§8f #3/#4): phantoms, the pinned noise
+    stream, generate(), and the reference's own on-disk files (dataset and
+    saddle directories, convergence CSV, PGM) written by its experiment_io."""
+    import shutil
+
+    from mctomo import experiment_io as rio
+    from mctomo.simulate import NoiseModel, nonrigid_preset, rigid_preset
+    from mctomo.solvers import SaddlePoint
+
+    out = {}
+    for kind in ("nested_shells", "thorax"):
+        for shape in ((48, 40), (64, 64), (17, 33)):
+            out[f"phantom_{kind}_{shape[0]}x{shape[1]}"] = make_phantom(kind, *shape)
+    for name, (shape, seed, gate) in {"f_5x7": ((5, 7), 1234, 3), "f_odd": ((1, 13), 7, 0),
+                                      "f_one": ((1, 1), 9, 2),
+                                      "f_big": ((128, 129), (1 << 64) + 5, 11)}.items():
+        out[name] = gaussian_field(shape, seed, gate)
+    tiny = Geometry(24, 24, 16, 32, math.hypot(24, 24) / 32)
+    ph = make_phantom("nested_shells", 24, 24)
+    cases = {"gen_rigid": (ph, motion_sequence("rigid", 4, 0.6), None, 3),
+             "gen_rigid_clean": (ph, motion_sequence("rigid", 4, 0.6), NoiseModel(0.0), 0),
+             "gen_dil": (make_phantom("thorax", 24, 24), motion_sequence("dilatation", 3, 0.8),
+                         NoiseModel(0.4), 5)}
+    for name, (phantom, motion, noise, seed) in cases.items():
+        ds = generate(phantom, motion, tiny, noise, master_seed=seed)
+        out[f"{name}_sinos"] = np.stack(ds.sinograms)
+        out[f"{name}_sigma"] = np.float64(ds.sigma)
+    for name, fn in (("preset_rigid", rigid_preset), ("preset_nonrigid", nonrigid_preset)):
+        ds = fn(size="fast", seed=1, magnitude=0.3)
+        out[f"{name}_sinos"] = np.stack(ds.sinograms[:3])  # first gates (fixture size)
+        out[f"{name}_sigma"] = np.float64(ds.sigma)
+        out[f"{name}_truth"] = ds.truth
+    # on-disk formats
+    io_dir = HERE / "io"
+    shutil.rmtree(io_dir, ignore_errors=True)
+    io_dir.mkdir()
+    ds = generate(ph, motion_sequence("rigid", 4, 0.6), tiny, None, master_seed=3,
+                  phantom_kind="nested_shells", magnitude=0.6)
+    rio.save_dataset(ds, io_dir / "dataset", norms={"gate_norms": [1.5, 2.25, 3.0, 3.5],
+                                                     "stacked_norm_sq": 12.5})
+    rng = np.random.default_rng(5)
+    saddle = SaddlePoint(x_star=rng.standard_normal((24, 24)),
+                         y_star=[rng.standard_normal((16, 32)) for _ in range(4)],
+                         source="cg", converged=True, residual=3.25e-9)
+    rio.save_saddle(io_dir / "saddle", saddle, meta={"alpha": 0.01, "iterations": 41})
+    rec = rio.ConvergenceRecord()
+    for k in range(1, 13):
+        rec.append(k, 0.7 ** k * (1.0 + 0.01 * math.sin(k)), 10.0 / k, float("nan") if k == 3
+                   else 0.1 / k, 4 * k, 4 * k)
+    rec.write_csv(io_dir / "record.csv")
+    fit = rio.fit_rate(rec)
+    out["fit_rate"] = np.array([fit.rate, fit.log_intercept, fit.r_squared, *fit.epoch_window])
+    fit2 = rio.fit_rate(rec, window=(2.0, 9.0))
+    out["fit_rate_window"] = np.array([fit2.rate, fit2.log_intercept, fit2.r_squared,
+                                       *fit2.epoch_window])
+    rio.write_pgm16(io_dir / "image.pgm", rng.standard_normal((7, 5)))
+    rio.write_pgm16(io_dir / "flat.pgm", np.full((3, 4), 2.5))
+    np.savez_compressed(HERE / "datasets.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["projector", "warps", "sampling", "tiny", "c1"]
+    which = sys.argv[1:] or ["projector", "warps", "sampling", "tiny", "c1", "datasets"]
     for w in which:
         t0 = time.time()
         {"projector": projector_cases, "warps": warp_cases, "sampling": sampling_cases,
-         "tiny": solver_tiny, "c1": solver_c1}[w]()
+         "tiny": solver_tiny, "c1": solver_c1, "datasets": dataset_cases}[w]()
         print(f"{w}: {time.time() - t0:.1f}s", flush=True)
