@@ -90,7 +90,7 @@ FwdArgs fwd_args(const mct_ray_plan* rp, const void* ws) {
     a.off_dy = rp->off_dy;
     a.off_part = rp->off_part;
     a.off_cnt = rp->off_cnt;
-    a.ksplit = MCT_KSPLIT;
+    a.ksplit = rp->ksplit1;
     a.wy = rp->wy;
     a.pb = rp->pb;
     return a;
@@ -244,7 +244,8 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     p->img_slot_bytes = align256((size_t)rows * cols * sizeof(float));
     off += p->img_slot_bytes * MCT_MAX_ASPLIT;
     p->off_part = off;
-    off += align256((size_t)MCT_KSPLIT * num_angles * num_bins * sizeof(double));
+    p->ksplit1 = choose_ksplit(num_angles, num_bins, std::max(rows, cols));
+    off += align256((size_t)p->ksplit1 * num_angles * num_bins * sizeof(double));
     p->off_cnt = off;
     off += align256((size_t)((num_angles + MCT_FWD_ANGLES - 1) / MCT_FWD_ANGLES) *
                     ((num_bins + 31) / 32) * sizeof(int));
@@ -619,7 +620,7 @@ int mct_iter_forward_dual(const mct_family* fam, const mct_items* it, mct_state*
     MCT_REQUIRE(fam->params_set, "mct_family_set_params has not been called");
     MCT_REQUIRE(s && s->y && s->d && ws, "null state buffer");
     FwdArgs fa = fwd_args(fam->ray, ws);
-    fa.ksplit = it->items_per_slice > 1 ? 1 : MCT_KSPLIT;  // see MCT_KSPLIT
+    fa.ksplit = it->items_per_slice > 1 ? 1 : fam->ray->ksplit1;  // see MCT_KSPLIT_MIN
     fa.sel = make_sel(it);
     fa.N = fam->N;
     fa.y = s->y;

@@ -41,7 +41,12 @@ struct AdjAngle {
 // A^* splits its angle loop over up to MCT_MAX_ASPLIT blocks per tile when one
 // launch has too few tiles to fill 148 SMs (single-gate SPDHG); each split
 // writes its own partial image slot and K4 sums the slots in a fixed order.
-#define MCT_MAX_ASPLIT 8
+#ifndef MCT_MAX_ASPLIT
+#define MCT_MAX_ASPLIT 16
+#endif
+#ifndef MCT_ASPLIT_MIN_PAIRS
+#define MCT_ASPLIT_MIN_PAIRS 8
+#endif
 
 struct mct_ray_plan {
     int rows, cols, A, B;
@@ -52,15 +57,23 @@ struct mct_ray_plan {
     RayAngle* d_fwd;
     AdjAngle* d_adj;
     size_t off_x, off_xt, off_dy, off_img, img_slot_bytes, off_part, off_cnt, item_bytes;
+    int ksplit1;  // K2 ray split of single-gate launches (see MCT_KSPLIT_MIN)
 };
 
-// K2 may split every ray's sample walk into ksplit <= MCT_KSPLIT consecutive
-// parts handled by different blocks (shorter blocks -> better load balance of
-// single-gate SPDHG launches); the last block of a tile to finish sums the fp64
-// partials in part order and runs the epilogue.  ksplit = 2 exactly when a
-// launch carries one gate per slice, so a batch of slices and a single slice
+// K2 may split every ray's sample walk into ksplit consecutive parts handled by
+// different blocks (shorter blocks -> better load balance of single-gate SPDHG
+// launches); the last block of a tile to finish sums the fp64 partials in part
+// order and runs the epilogue.  A launch whose slices carry one gate each uses
+// the plan's ksplit1 (enough parts to fill about one wave of resident blocks,
+// clamped to [MCT_KSPLIT_MIN, MCT_KSPLIT_MAX]); several gates per slice use 1.
+// ksplit1 depends only on the plan, so a batch of slices and a single slice
 // (or PDHG and a full-draw SPDHG step) run bitwise-identical arithmetic.
-#define MCT_KSPLIT 2
+#ifndef MCT_KSPLIT_MIN
+#define MCT_KSPLIT_MIN 2
+#endif
+#ifndef MCT_KSPLIT_MAX
+#define MCT_KSPLIT_MAX 4
+#endif
 #define MCT_FWD_ANGLES 4
 
 // --------------------------------------------------------------- warp plan --
@@ -190,6 +203,7 @@ cudaError_t launch_pad_sino(const float* sino, const AdjAngle* ang, char* ws, si
 cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st);
 cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, cudaStream_t st);
 int choose_asplit(const mct_ray_plan* rp, int items);
+int choose_ksplit(int A, int B, int n);
 cudaError_t launch_update(const UpdArgs& a, int mode, int slices, cudaStream_t st);
 cudaError_t launch_z_update(long long n, const float* dz, float* z, float* zbar, float theta,
                             cudaStream_t st);

@@ -15,11 +15,16 @@ namespace {
 // into the padded row-major X2 and transposed XT2 of the item workspace in the
 // "value + forward difference" pair layout: X2[r][c] = (W[r][c], W[r][c+1] -
 // W[r][c]) (zero outside the image), so a Joseph sample is one 8-byte load and
-// one FMA, v.x + frac * v.y.  A 32x32 tile plus a one-pixel halo of W is built
-// in shared memory, then both layouts are stored coalesced.
+// one FMA, v.x + frac * v.y.  A TxT tile plus a one-pixel halo of W is built in
+// shared memory, then both layouts are stored coalesced.  Multi-gate launches
+// use 32x32 tiles (4 elements per thread); single-gate launches 16x16 tiles with
+// one halo element per thread, so the warp's dependent load chain is paid once
+// per thread on a small grid.  Same per-element arithmetic (bitwise equal).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) pack_kernel(PackArgs p) {
-    __shared__ float tile[33][34];
+template <int T, int THREADS>
+__global__ void __launch_bounds__(THREADS) pack_kernel(PackArgs p) {
+    constexpr int H = T + 1;
+    __shared__ float tile[H][H + 1];
     const int item = blockIdx.z;
     int slice, gate, iter;
     resolve_item(p.sel, item, slice, gate, iter);
@@ -48,17 +53,17 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs p) {
     float2* X = reinterpret_cast<float2*>(base + p.off_x) + MCT_PADX;
     float2* XT = reinterpret_cast<float2*>(base + p.off_xt) + MCT_PADX;
 
-    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
-    const int tid = threadIdx.y * 32 + threadIdx.x;
+    const int c0 = blockIdx.x * T, r0 = blockIdx.y * T;
+    const int tid = threadIdx.x;
     const bool writer = prox && k_in_slice == 0 && p.x_next != nullptr;
     bool bad = false;
-    for (int idx = tid; idx < 33 * 33; idx += 256) {
-        const int i = idx / 33, jj = idx - i * 33;
+    for (int idx = tid; idx < H * H; idx += THREADS) {
+        const int i = idx / H, jj = idx - i * H;
         const int r = r0 + i, c = c0 + jj;
         float w = 0.0f;
         if (r < rows && c < cols) {
             w = ident ? xnew(r, c) : warp_apply_at(wd, r, c, xnew);
-            if (writer && i < 32 && jj < 32) {
+            if (writer && i < T && jj < T) {
                 const float xn = xnew(r, c);
                 p.x_next[(long long)slice * p.x_slice_stride + (long long)r * cols + c] = xn;
                 bad |= !isfinite(xn);
@@ -70,10 +75,9 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs p) {
         if ((threadIdx.x & 31) == 0) atomicMin(p.status, (unsigned long long)iter);
     }
     __syncthreads();
-    const int tx = threadIdx.x, ty = threadIdx.y;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int i = ty + 8 * k;
+    for (int o = tid; o < T * T; o += THREADS) {
+        const int i = o / T, tx = o - i * T;
         const int r = r0 + i, c = c0 + tx;
         if (r < rows && c < cols) {
             const float w = tile[i][tx];
@@ -520,8 +524,13 @@ __global__ void __launch_bounds__(ADJ_THREADS, ADJ_MIN_BLOCKS) adj_kernel(AdjArg
 }  // namespace
 
 cudaError_t launch_pack(const PackArgs& a, int items, cudaStream_t st) {
-    dim3 block(32, 8), grid((a.cols + 31) / 32, (a.rows + 31) / 32, items);
-    pack_kernel<<<grid, block, 0, st>>>(a);
+    if (items == 1) {  // single gate: small tiles, one halo element per thread
+        dim3 grid((a.cols + 15) / 16, (a.rows + 15) / 16, items);
+        pack_kernel<16, 320><<<grid, 320, 0, st>>>(a);
+    } else {
+        dim3 grid((a.cols + 31) / 32, (a.rows + 31) / 32, items);
+        pack_kernel<32, 256><<<grid, 256, 0, st>>>(a);
+    }
     return cudaGetLastError();
 }
 
@@ -531,6 +540,27 @@ cudaError_t launch_pad_sino(const float* sino, const AdjAngle* ang, char* ws, si
     dim3 block(256), grid((B + 255) / 256, A, items);
     pad_sino_kernel<<<grid, block, 0, st>>>(sino, ang, ws, item_bytes, off_dy, A, B, wy, pb);
     return cudaGetLastError();
+}
+
+int choose_ksplit(int A, int B, int n) {
+    static int slots = 0;  // resident fwd blocks per GPU (queried once)
+    if (slots == 0) {
+        int dev = 0, sms = 148, per_sm = FWD_MIN_BLOCKS;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fwd_kernel<1>, 32 * FWD_ANGLES,
+                                                          0) != cudaSuccess ||
+            per_sm < 1)
+            per_sm = FWD_MIN_BLOCKS;
+        slots = sms * per_sm;
+    }
+    const long long blocks = (long long)((B + 31) / 32) * ((A + FWD_ANGLES - 1) / FWD_ANGLES);
+    long long k = (slots + blocks - 1) / blocks;
+    const long long by_len = n / 16 > 1 ? n / 16 : 1;  // >= 16 samples per part
+    k = k < by_len ? k : by_len;
+    k = k > MCT_KSPLIT_MAX ? MCT_KSPLIT_MAX : k;
+    k = k < MCT_KSPLIT_MIN ? MCT_KSPLIT_MIN : k;
+    return (int)k;
 }
 
 cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st) {
@@ -564,7 +594,9 @@ int choose_asplit(const mct_ray_plan* rp, int items) {
     long long s = tiles >= slots ? 1 : slots / tiles;
     s = s < 1 ? 1 : s;
     s = s > MCT_MAX_ASPLIT ? MCT_MAX_ASPLIT : s;
-    const long long by_angles = rp->A / 32 > 0 ? rp->A / 32 : 1;  // >= 16 pairs per split
+    // >= MCT_ASPLIT_MIN_PAIRS angle pairs per split
+    const long long by_angles =
+        rp->A / (2 * MCT_ASPLIT_MIN_PAIRS) > 0 ? rp->A / (2 * MCT_ASPLIT_MIN_PAIRS) : 1;
     return (int)(s < by_angles ? s : by_angles);
 }
 
