@@ -22,6 +22,10 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs p) {
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n) return;
     const int qr = (int)(q / p.cols), qc = (int)(q - (long long)qr * p.cols);
+    const long long o = (long long)slice * n + q;
+    // state loads issued ahead of the gather's dependent chain
+    const float z0 = MODE == 1 ? p.z[o] : 0.0f;
+    const float xn = MODE != 0 ? __ldg(p.x_next + o) : 0.0f;
     float sum = 0.0f, wsum = 0.0f;
     for (int k = 0; k < p.sel.ips; ++k) {
         const int item = slice * p.sel.ips + k;
@@ -32,11 +36,20 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs p) {
                               : p.ws + (size_t)item * p.item_bytes + p.off_img;
         const int asplit = p.asplit;
         const size_t slot = p.img_slot_bytes;
-        // sum of the adjoint's partial-image slots, fixed order
+        // sum of the adjoint's partial-image slots, fixed order (loads four at a time)
         auto fetch = [&](long long e) -> float {
             float v = __ldg(reinterpret_cast<const float*>(img) + e);
-            for (int s = 1; s < asplit; ++s)
-                v += __ldg(reinterpret_cast<const float*>(img + s * slot) + e);
+            for (int s = 1; s < asplit; s += 4) {
+                float t[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    t[j] = s + j < asplit
+                               ? __ldg(reinterpret_cast<const float*>(img + (s + j) * slot) + e)
+                               : 0.0f;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (s + j < asplit) v += t[j];
+            }
             return v;
         };
         float v;
@@ -49,17 +62,16 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs p) {
         sum += v;
         if (MODE == 1) wsum = fmaf(p.gp[gate].theta_over_p, v, wsum);
     }
-    const long long o = (long long)slice * n + q;
     if (MODE == 0) {
         p.out[o] = sum;
     } else if (MODE == 1) {
-        const float zq = p.z[o] + sum;
+        const float zq = z0 + sum;
         p.z[o] = zq;
         p.zbar[o] = zq + wsum;
-        p.x[o] = p.x_next[o];
+        p.x[o] = xn;
     } else {
         p.dz[o] = sum;
-        p.x[o] = p.x_next[o];
+        p.x[o] = xn;
     }
 }
 

@@ -97,6 +97,22 @@ __device__ __forceinline__ float warp_adjoint_at(const WarpDesc& w, Fetch fetch,
     if (w.kind == MCT_WARP_IDENTITY) return fetch(q);
     const int e0 = __ldg(w.tptr + q), e1 = __ldg(w.tptr + q + 1);
     float acc = 0.0f;
-    for (int e = e0; e < e1; ++e) acc = fmaf(__ldg(w.tw + e), fetch(__ldg(w.tidx + e)), acc);
+    // four entries per round: their index / weight loads, then their fetches, are
+    // in flight together; the FMAs stay in entry order (same sum as one by one)
+    for (int e = e0; e < e1; e += 4) {
+        int idx[4];
+        float wt[4], v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool ok = e + j < e1;
+            idx[j] = ok ? __ldg(w.tidx + e + j) : -1;
+            wt[j] = ok ? __ldg(w.tw + e + j) : 0.0f;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = idx[j] >= 0 ? fetch(idx[j]) : 0.0f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (idx[j] >= 0) acc = fmaf(wt[j], v[j], acc);
+    }
     return acc;
 }
