@@ -12,8 +12,8 @@ from .experiment_io import (ConvergenceRecord, RasterFormatError, RateFit, fit_r
                             load_dataset, load_saddle, read_raster, rmse, save_dataset,
                             save_saddle, write_raster)
 from .functionals import fit_value, g_value, moduli, prox_fstar, prox_g
-from .linops import (ComposedMap, GramSumMap, LinearMap, adjoint_mismatch, compose,
-                     power_method, stacked_norm_sq)
+from .linops import (ComposedMap, DiagonalMap, GramSumMap, IdentityMap, LinearMap, StackedMap,
+                     adjoint_mismatch, compose, power_method, stacked_norm_sq)
 from .motion import DenseWarpOperator, MotionParams, WarpOperator, motion_sequence
 from .projector import Geometry, GatedOperator, RayTransform, adjoint, forward, ray_transform
 from .simulate import (PHANTOM_KINDS, GatedDataset, NoiseModel, estimate_norms, gate_operators,

@@ -30,6 +30,9 @@ from . import _lib
 
 __all__ = [
     "LinearMap",
+    "IdentityMap",
+    "DiagonalMap",
+    "StackedMap",
     "ComposedMap",
     "GramSumMap",
     "compose",
@@ -110,6 +113,80 @@ class LinearMap(ABC):
         if t.dtype != torch.float32:
             t = t.float()
         return t.contiguous()
+
+
+class IdentityMap(LinearMap):
+    """Identity on a grid (reference linops.py:76-87); a device copy."""
+
+    def __init__(self, shape):
+        self.domain_shape = tuple(int(n) for n in shape)
+        self.range_shape = self.domain_shape
+
+    def apply_device(self, x):
+        return x.clone()
+
+    def adjoint_device(self, y):
+        return y.clone()
+
+
+class DiagonalMap(LinearMap):
+    """Elementwise multiplication by a fixed array, self-adjoint (linops.py:90-102).
+
+    The diagonal lives on the device in fp32.
+    """
+
+    def __init__(self, diag):
+        self.diag = np.asarray(diag, dtype=np.float64).copy()
+        self.domain_shape = self.diag.shape
+        self.range_shape = self.diag.shape
+        self._dev = None
+
+    def _d(self):
+        if self._dev is None:
+            torch = _lib.require_cuda()
+            self._dev = torch.from_numpy(self.diag.astype(np.float32)).cuda()
+        return self._dev
+
+    def apply_device(self, x):
+        return x * self._d()
+
+    def adjoint_device(self, y):
+        return y * self._d()
+
+
+class StackedMap(LinearMap):
+    """Row stack of maps sharing one domain and one range (linops.py:135-169).
+
+    ``apply`` stacks the block outputs along a new leading axis; ``adjoint_apply``
+    sums the block adjoints in block order (device axpby, fixed order).
+    """
+
+    def __init__(self, blocks: Sequence[LinearMap]):
+        blocks = tuple(blocks)
+        if not blocks:
+            raise ValueError("StackedMap needs at least one block")
+        dom, rng = tuple(blocks[0].domain_shape), tuple(blocks[0].range_shape)
+        for k, b in enumerate(blocks):
+            if tuple(b.domain_shape) != dom:
+                raise ValueError(f"block {k} domain {tuple(b.domain_shape)} != {dom}")
+            if tuple(b.range_shape) != rng:
+                raise ValueError(f"block {k} range {tuple(b.range_shape)} != {rng}")
+        self.blocks = blocks
+        self.domain_shape = dom
+        self.range_shape = (len(blocks),) + rng
+
+    def apply_device(self, x):
+        torch = _lib.require_cuda()
+        return torch.stack([b.apply_device(x) for b in self.blocks])
+
+    def adjoint_device(self, y):
+        L = _lib.load()
+        out = self.blocks[0].adjoint_device(y[0].contiguous()).clone()
+        for b, yk in zip(self.blocks[1:], y[1:]):
+            g = b.adjoint_device(yk.contiguous())
+            _lib.check(L.mct_axpby(out.numel(), 1.0, _lib.ptr(g), 1.0, _lib.ptr(out),
+                                   _lib.stream_handle()))
+        return out
 
 
 class ComposedMap(LinearMap):

@@ -314,3 +314,28 @@ def test_dense_zero_field_is_identity_and_out_of_frame(m, rng):
         m.DenseWarpOperator(np.full((2, 4, 4), np.nan, dtype=np.float32))
     with pytest.raises(ValueError):
         m.DenseWarpOperator(np.zeros((3, 4, 4)))
+
+
+def test_helper_maps_on_device(m, rng):
+    """IdentityMap, DiagonalMap, StackedMap of gated operators (linops.py:76-169)."""
+    geom = m.Geometry(24, 24, 16, 32, 1.1)
+    ops = m.gate_operators(geom, [m.MotionParams.identity(),
+                                  m.MotionParams(kind="rigid", rotation=0.2, translation=(1.0, -0.5)),
+                                  m.MotionParams(kind="dilatation", scale=1.05)])
+    x = rng.standard_normal(geom.image_shape).astype(np.float32).astype(np.float64)
+    ident = m.IdentityMap(geom.image_shape)
+    assert np.array_equal(ident.apply(x), x)
+    d = rng.uniform(0.5, 2.0, geom.image_shape).astype(np.float32).astype(np.float64)
+    assert np.allclose(m.DiagonalMap(d).apply(x), x * d, rtol=1e-6)
+    st = m.StackedMap(ops)
+    y = st.apply(x)
+    assert y.shape == (3,) + tuple(geom.sino_shape)
+    for k, op in enumerate(ops):
+        assert np.array_equal(y[k], op.apply(x))
+    yy = rng.standard_normal(st.range_shape).astype(np.float32).astype(np.float64)
+    want = sum(op.adjoint_apply(yy[k]).astype(np.float64) for k, op in enumerate(ops))
+    assert rel_l2(st.adjoint_apply(yy), want) <= 1e-6
+    assert m.adjoint_mismatch(st, pairs=3) <= TOL
+    # ||stack||^2 == lambda_max(sum_i A_i^* A_i)  (linops.py:275-289)
+    nsq = m.power_method(st, iterations=60) ** 2
+    assert nsq == pytest.approx(m.stacked_norm_sq(ops, iterations=60), rel=1e-4)

@@ -173,3 +173,25 @@ def test_no_cpu_fallback():
 
     with pytest.raises(RuntimeError, match="CUDA"):
         RayTransform(Geometry(8, 8, 4, 12, 1.0)).apply(np.zeros((8, 8)))
+
+
+def test_helper_maps_validation_and_no_fallback():
+    """IdentityMap / DiagonalMap / StackedMap (linops.py:76-169): shape checks on
+    the host, compute only on the device."""
+    torch = pytest.importorskip("torch")
+    from paper_2410_10503_b200 import DiagonalMap, IdentityMap, StackedMap
+
+    a, b = IdentityMap((3, 4)), IdentityMap((3, 5))
+    with pytest.raises(ValueError):
+        StackedMap([])
+    with pytest.raises(ValueError):
+        StackedMap([a, b])
+    with pytest.raises(ValueError):
+        StackedMap([a, DiagonalMap(np.ones((4, 3)))])
+    s = StackedMap([a, DiagonalMap(np.full((3, 4), 2.0))])
+    assert s.domain_shape == (3, 4) and s.range_shape == (2, 3, 4)
+    with pytest.raises(ValueError):
+        s.apply(np.zeros((4, 3)))
+    if not torch.cuda.is_available():
+        with pytest.raises(RuntimeError, match="CUDA"):
+            s.apply(np.zeros((3, 4)))
