@@ -51,7 +51,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
                     help="use the torch.distributed gate-sharded path even for one rank "
-                         "(exercises the NCCL code path on a single GPU)")
+                         "(exercises the multi-GPU code path on a single GPU)")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="gate-sharded PDHG partial sum: fused NVLink peer-memory exchange "
+                         "inside the z update (p2p) or NCCL allreduce + z update")
     return ap.parse_args()
 
 
@@ -292,24 +295,40 @@ def run_ours(args, cfg):
     import ctypes
 
     L = _lib.load()
+    exchange = None
     if not use_dist:
         eng = Engine([problem.operators], [problem.data])
         worker = None
     else:
-        worker = ShardedPDHG(pcfg, problem, rank, world)
+        exchange = args.exchange
+        try:
+            worker = ShardedPDHG(pcfg, problem, rank, world, exchange=exchange)
+        except Exception as exc:  # no symmetric-memory / P2P support on this box
+            if exchange != "p2p":
+                raise
+            print(json.dumps({"warning": f"p2p exchange unavailable ({exc}); using nccl"}),
+                  file=sys.stderr)
+            exchange = "nccl"
+            worker = ShardedPDHG(pcfg, problem, rank, world, exchange=exchange)
         eng = worker.engine
     eng.set_params(pcfg)
     eng.reset()
     items = eng.items_pdhg(epoch_ctr=True)
     ip, sp = ctypes.byref(items), ctypes.byref(eng._st)
     fam, ws, st = eng.family.handle, _lib.ptr(eng.ws), _lib.stream_handle(stream)
-    dzp = _lib.ptr(worker.dz) if use_dist else None
     names = ["K1_prox_warp", "K2_forward_dual", "K3_adjoint", "K4_adjoint_update"]
+    dz_now = [None]
+
+    def k4():
+        dz_now[0] = worker.partial_buffer() if use_dist else None
+        _lib.check(L.mct_iter_adjoint_update(fam, ip, sp, _lib.ptr(dz_now[0]) if use_dist
+                                             else None, ws, st))
+
     calls = [
         lambda: _lib.check(L.mct_iter_prox_warp(fam, ip, sp, eng.tau, problem.alpha, ws, st)),
         lambda: _lib.check(L.mct_iter_forward_dual(fam, ip, sp, ws, st)),
         lambda: _lib.check(L.mct_iter_adjoint(fam, ip, ws, st)),
-        lambda: _lib.check(L.mct_iter_adjoint_update(fam, ip, sp, dzp, ws, st)),
+        k4,
     ]
 
     def step_fn(evs=None):
@@ -320,11 +339,10 @@ def run_ours(args, cfg):
         if evs is not None:
             evs[4].record(stream)
         if use_dist:
-            dist.all_reduce(worker.dz, op=dist.ReduceOp.SUM)
-            eng.z_update(worker.dz, pcfg.theta)
+            worker.reduce_update(dz_now[0])
         eng.advance_epoch()
 
-    launches_per_step = 6 if use_dist else 5
+    launches_per_step = (7 if exchange == "p2p" else 6) if use_dist else 5
     for _ in range(args.warmup):
         step_fn()
     hbm_peak, peak_src = peaks()
@@ -339,6 +357,8 @@ def run_ours(args, cfg):
         end.record(stream)
         barrier()
     ms_total = max_over_ranks(start.elapsed_time(end))
+    if use_dist:
+        worker.check()  # a timed-out peer wait raises instead of reporting a number
     primal, dual = eng.read_status()
     if primal is not None or dual is not None:
         print(json.dumps({"warning": "non-finite iterate during the timed run",
@@ -448,6 +468,7 @@ def run_ours(args, cfg):
                                    f"(peak {cfg.peak} px), {cfg.num_angles}x{cfg.num_bins} bins, "
                                    f"alpha={cfg.alpha}, PDHG gate-sharded over {world} GPU(s)",
                        "mode": "pdhg", "parallelism": f"gate-shard x{world}",
+                       "exchange": (exchange if use_dist else "none (single process)"),
                        "l2": "per-epoch working set ~200 MB > 126 MB L2 (no flush needed)"},
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved,
                          "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,

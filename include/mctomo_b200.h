@@ -229,6 +229,26 @@ int mct_axpby_mixed(long long n, double alpha, const void* x_dev, int x_is_f64, 
 int mct_dot_f64(const double* a_dev, const double* b_dev, long long n, double* out_dev,
                 double* scratch_dev, void* stream);
 
+/* --------------------------------------------- fused multi-GPU exchange */
+/* Gate-sharded PDHG without a collective library: the partial
+ * dz_r = sum_{i in gates(r)} D_i^* A_i^* dy_i that mct_iter_adjoint_update
+ * (dz_partial) wrote into this rank's peer-visible buffer is combined over
+ * NVLink peer memory inside the z / z-bar update (solvers.py:356-366).
+ *   pads_dev  : device array of `world` pointers, pads_dev[q] = rank q's signal
+ *               pad (world uint64 slots, zeroed before the first epoch; slot r
+ *               holds the last epoch rank r posted);
+ *   parts_dev : device array of `world` pointers to the ranks' partial buffers
+ *               of this epoch's parity (n floats each).
+ * mct_exchange_post publishes this rank's partial for `epoch` (>= 1, strictly
+ * increasing); mct_exchange_z_update waits for every rank's post of `epoch`
+ * and applies z += sum_q parts[q], zbar = z + theta * sum_q parts[q], summing
+ * in rank order (the same bits on every rank).  The wait is bounded: on expiry
+ * *failed_dev is set to 1 and z / zbar are left untouched.                    */
+int mct_exchange_post(void* const* pads_dev, int world, int rank, uint64_t epoch, void* stream);
+int mct_exchange_z_update(const float* const* parts_dev, const uint64_t* my_pad_dev, int world,
+                          uint64_t epoch, long long n, float* z_dev, float* zbar_dev, double theta,
+                          unsigned int* failed_dev, void* stream);
+
 /* ------------------------------------------------------------ data generation */
 /* Seeded Gaussian sinogram noise on the device, the documented recipe of
  * simulate.gaussian_field (simulate.py:113-133) used by simulate.generate

@@ -719,6 +719,30 @@ int mct_dot_f64(const double* a, const double* b, long long n, double* out, doub
     return MCT_OK;
 }
 
+// --------------------------------------------------- fused multi-GPU exchange
+int mct_exchange_post(void* const* pads, int world, int rank, uint64_t epoch, void* stream) {
+    MCT_REQUIRE(pads, "null pad array");
+    MCT_REQUIRE(world >= 1 && world <= 1024 && rank >= 0 && rank < world, "invalid world / rank");
+    MCT_REQUIRE(epoch >= 1, "epoch must be >= 1");
+    MCT_CUDA(launch_exchange_post(reinterpret_cast<unsigned long long* const*>(pads), world, rank,
+                                  (unsigned long long)epoch, (cudaStream_t)stream),
+             "exchange post");
+    return MCT_OK;
+}
+
+int mct_exchange_z_update(const float* const* parts, const uint64_t* my_pad, int world,
+                          uint64_t epoch, long long n, float* z, float* zbar, double theta,
+                          unsigned int* failed, void* stream) {
+    MCT_REQUIRE(parts && my_pad && z && zbar && failed, "null argument");
+    MCT_REQUIRE(world >= 1 && world <= 1024, "invalid world size");
+    MCT_REQUIRE(epoch >= 1 && n >= 0, "epoch must be >= 1 and n >= 0");
+    MCT_CUDA(launch_exchange_update(parts, reinterpret_cast<const unsigned long long*>(my_pad),
+                                    world, (unsigned long long)epoch, n, z, zbar, (float)theta,
+                                    failed, (cudaStream_t)stream),
+             "exchange z update");
+    return MCT_OK;
+}
+
 // ------------------------------------------------------------ data generation
 int mct_gaussian_field(uint64_t key0, uint64_t key1, long long count, double scale,
                        const float* base, void* out, int out_is_f64, void* stream) {

@@ -227,5 +227,12 @@ cudaError_t launch_gaussian_field(unsigned long long k0, unsigned long long k1, 
                                   double scale, const float* base, void* out, int out_f64,
                                   cudaStream_t st);
 
+cudaError_t launch_exchange_post(unsigned long long* const* pads, int world, int rank,
+                                 unsigned long long epoch, cudaStream_t st);
+cudaError_t launch_exchange_update(const float* const* parts, const unsigned long long* my_pad,
+                                   int world, unsigned long long epoch, long long n, float* z,
+                                   float* zbar, float theta, unsigned int* failed,
+                                   cudaStream_t st);
+
 // error reporting (abi.cu)
 int mct_set_error(int code, const std::string& msg);

@@ -2,9 +2,13 @@
 
 * PDHG gate-sharding: rank r owns a contiguous block of gates (their y_i, d_i,
   warps); every rank holds the replicated x, z, zbar and computes the identical
-  prox step locally, so the only exchange per iteration is one allreduce(sum)
-  of the image-sized partial sum of D_i^* A_i^* dy_i (NCCL over NVLink), after
-  which every rank applies z += dz, zbar = z + theta*dz (all p_i = 1 in PDHG).
+  prox step locally, so the only exchange per iteration is the sum of the
+  image-sized partials D_i^* A_i^* dy_i, after which every rank applies
+  z += dz, zbar = z + theta*dz (all p_i = 1 in PDHG).  Two exchanges:
+  ``"p2p"`` (default on GPUs) — K4 writes the partial into a peer-visible
+  symmetric buffer and the fused ``mct_exchange_*`` kernels sum the peers'
+  partials over NVLink inside the z update (``P2PExchange``); ``"nccl"`` — an
+  NCCL allreduce(sum) followed by ``mct_iter_z_update``.
 * Batch slices (C5): independent units, ``slice_shard`` splits them with no
   data-path collective.
 * SPDHG of a single problem does not shard (one gate per iteration,
@@ -17,7 +21,8 @@ from typing import Protocol
 
 import numpy as np
 
-__all__ = ["gate_shard", "slice_shard", "sharded_epochs", "ShardedPDHG", "run_pdhg_sharded"]
+__all__ = ["gate_shard", "slice_shard", "sharded_epochs", "ShardedPDHG", "run_pdhg_sharded",
+           "P2PExchange", "exchange_schedule"]
 
 
 def _block(count: int, world: int, rank: int) -> tuple[int, int]:
@@ -38,6 +43,81 @@ def slice_shard(num_slices: int, world: int, rank: int) -> tuple[int, int]:
     return _block(num_slices, world, rank)
 
 
+def exchange_schedule(epoch: int) -> tuple[int, int]:
+    """(flag value, buffer parity) of the p2p exchange of PDHG iteration ``epoch``
+    (0-based): flags count from 1 (pads start zeroed) and the partial buffers
+    alternate, so a rank rewrites a buffer only after every peer has posted the
+    next iteration (see csrc/exchange_kernels.cu)."""
+    if epoch < 0:
+        raise ValueError("epoch must be >= 0")
+    return epoch + 1, (epoch + 1) % 2
+
+
+def _align(n: int, a: int = 256) -> int:
+    return (n + a - 1) // a * a
+
+
+class P2PExchange:
+    """Peer-memory exchange of gate-sharded PDHG partials (``mct_exchange_*``).
+
+    One symmetric allocation per rank holds two partial buffers (iteration
+    parity) and a signal pad of ``world`` uint64 slots; ``rendezvous`` maps every
+    peer's allocation into this process (NVLink / NVSwitch peer addresses).
+    """
+
+    def __init__(self, n: int, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        from . import _lib
+
+        self.torch, self._lib = torch, _lib
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.n = int(n)
+        part = _align(4 * self.n)
+        pad_off = 2 * part
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.buf = symm.empty(pad_off + _align(8 * self.world), dtype=torch.uint8, device=dev)
+        self.buf.zero_()
+        self.handle = symm.rendezvous(self.buf, self.group)
+        peers = [int(p) for p in self.handle.buffer_ptrs]
+        if len(peers) != self.world:
+            raise RuntimeError("symmetric-memory rendezvous returned a wrong peer count")
+        i64 = torch.int64
+        self.parts_dev = [torch.tensor([p + k * part for p in peers], dtype=i64, device=dev)
+                          for k in (0, 1)]
+        self.pads_dev = torch.tensor([p + pad_off for p in peers], dtype=i64, device=dev)
+        self.my_pad = self.buf.data_ptr() + pad_off
+        self.partials = [self.buf[k * part:k * part + 4 * self.n].view(torch.float32)
+                         for k in (0, 1)]
+        self.failed = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.epoch = 0  # iterations exchanged so far
+        torch.cuda.synchronize()
+        dist.barrier(self.group)  # every pad is zero before the first post
+
+    def partial(self):
+        """The buffer K4 writes this iteration's partial into."""
+        return self.partials[exchange_schedule(self.epoch)[1]]
+
+    def exchange(self, z, zbar, theta: float) -> None:
+        """Post this rank's partial, then z += sum_q partial_q, zbar = z + theta*sum."""
+        L, lib = self._lib.load(), self._lib
+        flag, parity = exchange_schedule(self.epoch)
+        st = lib.stream_handle()
+        lib.check(L.mct_exchange_post(lib.ptr(self.pads_dev), self.world, self.rank, flag, st))
+        lib.check(L.mct_exchange_z_update(lib.ptr(self.parts_dev[parity]), self.my_pad,
+                                          self.world, flag, self.n, lib.ptr(z), lib.ptr(zbar),
+                                          float(theta), lib.ptr(self.failed), st))
+        self.epoch += 1
+
+    def check(self) -> None:
+        if int(self.failed.item()):
+            raise RuntimeError("p2p exchange timed out waiting for a peer's partial")
+
+
 class ShardWorker(Protocol):
     def local_iteration(self):
         """Run the local gates of one PDHG iteration; return the partial dz tensor."""
@@ -47,12 +127,15 @@ class ShardWorker(Protocol):
 
 
 def sharded_epochs(worker: ShardWorker, epochs: int, group=None) -> None:
-    """PDHG epochs with one allreduce(sum) of the image-sized update per iteration."""
+    """PDHG epochs with one image-sized sum per iteration (allreduce, or the
+    worker's own p2p exchange inside ``finish``)."""
     import torch.distributed as dist
 
+    nccl = getattr(worker, "exchange", "nccl") == "nccl"
     for _ in range(epochs):
         dz = worker.local_iteration()
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        if (nccl and dist.is_available() and dist.is_initialized()
+                and dist.get_world_size(group) > 1):
             dist.all_reduce(dz, op=dist.ReduceOp.SUM, group=group)
         worker.finish(dz)
 
@@ -60,9 +143,12 @@ def sharded_epochs(worker: ShardWorker, epochs: int, group=None) -> None:
 class ShardedPDHG:
     """GPU worker: the fused K1..K4 kernels on the local gate block."""
 
-    def __init__(self, config, problem, rank: int, world: int, keep_projections=False):
+    def __init__(self, config, problem, rank: int, world: int, keep_projections=False,
+                 exchange: str = "nccl", group=None):
         from .engine import Engine
 
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError("exchange must be 'nccl' or 'p2p'")
         if config.mode != "pdhg":
             raise ValueError("gate sharding applies to pdhg (spdhg runs as replicas)")
         if config.num_gates != problem.num_gates:
@@ -76,27 +162,57 @@ class ShardedPDHG:
         self.engine.reset()
         self.alpha = problem.alpha
         self.theta = config.theta
-        self.dz = self.engine.torch.zeros_like(self.engine.x)
+        self.exchange = exchange
+        self.p2p = P2PExchange(self.engine.x.numel(), group) if exchange == "p2p" else None
+        self.dz = None if self.p2p else self.engine.torch.zeros_like(self.engine.x)
+
+    def partial_buffer(self):
+        """Where K4 writes this iteration's partial sum (shape of x)."""
+        return self.p2p.partial().view(self.engine.x.shape) if self.p2p else self.dz
 
     def local_iteration(self):
         eng = self.engine
-        eng.iteration(eng.items_pdhg(epoch_ctr=True), self.alpha, dz=self.dz)
-        return self.dz
+        dz = self.partial_buffer()
+        eng.iteration(eng.items_pdhg(epoch_ctr=True), self.alpha, dz=dz)
+        return dz
+
+    def reduce_update(self, dz, group=None):
+        """Sum the partials over the ranks and apply the z / z-bar update."""
+        if self.p2p:
+            self.p2p.exchange(self.engine.z, self.engine.zbar, self.theta)
+            return
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.all_reduce(dz, op=dist.ReduceOp.SUM, group=group)
+        self.engine.z_update(dz, self.theta)
 
     def finish(self, dz):
-        self.engine.z_update(dz, self.theta)
+        if self.p2p:
+            self.p2p.exchange(self.engine.z, self.engine.zbar, self.theta)
+        else:
+            self.engine.z_update(dz, self.theta)
         self.engine.advance_epoch()
 
+    def check(self):
+        if self.p2p:
+            self.p2p.check()
 
-def run_pdhg_sharded(config, problem, group=None):
-    """PDHG over the ranks of ``group``; returns x (float64 numpy) on every rank."""
+
+def run_pdhg_sharded(config, problem, group=None, exchange: str = "nccl"):
+    """PDHG over the ranks of ``group``; returns x (float64 numpy) on every rank.
+
+    ``exchange="p2p"`` needs an initialised NCCL process group (symmetric-memory
+    rendezvous); ``"nccl"`` also runs without one (single process).
+    """
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    w = ShardedPDHG(config, problem, rank, world)
+    w = ShardedPDHG(config, problem, rank, world, exchange=exchange, group=group)
     sharded_epochs(w, config.epochs, group)
     from .solvers import _raise_status
 
+    w.check()
     _raise_status(w.engine)
     return np.asarray(w.engine.x[0].double().cpu().numpy())

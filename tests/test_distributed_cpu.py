@@ -63,6 +63,37 @@ class OracleShardWorker:
         self.x = self.x_new
 
 
+class OracleP2PWorker(OracleShardWorker):
+    """The p2p protocol of distributed.P2PExchange, emulated on CPU: partials in
+    parity buffers, exchange = gather every rank's buffer of this parity and sum in
+    rank order inside the z update (the arithmetic of exchange_update_kernel)."""
+
+    exchange = "p2p"
+
+    def __init__(self, *a):
+        super().__init__(*a)
+        from paper_2410_10503_b200.distributed import exchange_schedule
+
+        self.schedule = exchange_schedule
+        self.bufs = [torch.zeros(self.x.shape, dtype=torch.float64) for _ in range(2)]
+        self.epoch = 0
+
+    def local_iteration(self):
+        dz = super().local_iteration()
+        buf = self.bufs[self.schedule(self.epoch)[1]]
+        buf.copy_(dz)
+        return buf
+
+    def finish(self, dz):
+        parts = [torch.zeros_like(dz) for _ in range(dist.get_world_size())]
+        dist.all_gather(parts, self.bufs[self.schedule(self.epoch)[1]])
+        s = parts[0].clone()
+        for q in parts[1:]:
+            s += q
+        super().finish(s)
+        self.epoch += 1
+
+
 def _problem():
     cfgw = workloads.WorkloadConfig("dist", 40, 36, 59, 5, "dense", 4, 1e-2, 6, peak=2.0)
     inp = workloads.slice_inputs(cfgw, 0)
@@ -76,13 +107,14 @@ def _problem():
     return cfg, cfgw.alpha, ops, data
 
 
-def _worker(rank, world, port, out_path):
+def _worker(rank, world, port, out_path, kind="nccl"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         cfg, alpha, ops, data = _problem()
-        w = OracleShardWorker(cfg, alpha, ops, data, rank, world)
+        cls = OracleP2PWorker if kind == "p2p" else OracleShardWorker
+        w = cls(cfg, alpha, ops, data, rank, world)
         sharded_epochs(w, cfg.epochs)
         if rank == 0:
             np.save(out_path, w.x)
@@ -98,12 +130,29 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_gate_sharded_pdhg_gloo_world2_matches_single_process(tmp_path):
+@pytest.mark.parametrize("kind", ["nccl", "p2p"])
+def test_gate_sharded_pdhg_gloo_world2_matches_single_process(tmp_path, kind):
     out = str(tmp_path / "x.npy")
-    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), out, kind), nprocs=2, join=True)
     x0 = np.load(out)
     x1 = np.load(out.replace(".npy", "_r1.npy"))
     assert np.array_equal(x0, x1)  # replicated primal stays identical on every rank
     cfg, alpha, ops, data = _problem()
     st, _ = osolver.run(cfg, alpha, ops, data, diagnostics=False)
     assert np.linalg.norm(x0 - st.x) <= 1e-12 * np.linalg.norm(st.x)
+
+
+def test_p2p_exchange_schedule():
+    """Flags start at 1 (pads are zeroed) and increase by one per iteration; the
+    partial buffers alternate, so a buffer is rewritten two iterations later —
+    after every peer has posted the iteration in between (exchange_kernels.cu)."""
+    from paper_2410_10503_b200.distributed import exchange_schedule
+
+    sched = [exchange_schedule(e) for e in range(6)]
+    assert [f for f, _ in sched] == [1, 2, 3, 4, 5, 6]
+    assert [p for _, p in sched] == [1, 0, 1, 0, 1, 0]
+    for e in range(4):
+        assert exchange_schedule(e)[1] == exchange_schedule(e + 2)[1]
+        assert exchange_schedule(e)[1] != exchange_schedule(e + 1)[1]
+    with pytest.raises(ValueError):
+        exchange_schedule(-1)

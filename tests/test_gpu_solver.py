@@ -200,6 +200,38 @@ def test_sharded_pdhg_single_rank_matches_run(m, golden_tiny):
     assert rel_l2(x_sh, G["pdhg__x"]) <= ITER_TOL if cfg.epochs == 10 else True
 
 
+def test_p2p_exchange_matches_nccl_single_rank(m, golden_tiny):
+    """The fused peer-memory exchange (mct_exchange_*) on a one-rank NCCL group:
+    same bits as allreduce + z update, flags advance, no timeout."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_10503_b200.distributed import ShardedPDHG, run_pdhg_sharded
+
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    cfg = tiny_config(m, G, "pdhg", 0, epochs=7)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                            world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        x_nccl = run_pdhg_sharded(cfg, problem, exchange="nccl")
+        x_p2p = run_pdhg_sharded(cfg, problem, exchange="p2p")
+        assert np.array_equal(x_p2p, x_nccl)
+        w = ShardedPDHG(cfg, problem, 0, 1, exchange="p2p")
+        for _ in range(3):
+            w.finish(w.local_iteration())
+        torch.cuda.synchronize()
+        pad = w.p2p.buf[-256:].view(torch.int64)[0].item()
+        assert pad == 3 and w.p2p.epoch == 3 and int(w.p2p.failed.item()) == 0
+    finally:
+        dist.destroy_process_group()
+
+
 def test_c2_shape_spdhg_trajectory_vs_oracle(m):
     """BASELINE C2 shape (256^2, 10 dense gates, 360x363): 2 SPDHG epochs vs the oracle."""
     from paper_2410_10503_b200 import workloads
