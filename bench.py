@@ -142,6 +142,9 @@ def alg_bytes(cfg):
             "elem": b_elem, "min_pair": b_min_pair, "S": S}
 
 
+TRAFFIC_ITEMS = 20  # items of the launch profiles/ncu_traffic.json was captured on
+
+
 def load_traffic():
     p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
@@ -372,6 +375,8 @@ def run_ours(args, cfg):
     iter_ms = sum(kern.values())
     dominant = max(("K2_forward_dual", "K3_adjoint"), key=lambda k: kern[k])
     traffic = load_traffic().get(dominant)
+    if traffic is not None:  # captured on the 20-item C3 launch: scale to this launch
+        traffic = traffic * items_per_launch / TRAFFIC_ITEMS
     achieved = ab[dominant] * items_per_launch / (kern[dominant] * 1e-3) / 1e9
     pair_gbs = ab["pair"] * items_per_launch / (iter_ms * 1e-3) / 1e9
     min_gbs = ab["min_pair"] * items_per_launch / (iter_ms * 1e-3) / 1e9
