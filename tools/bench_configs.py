@@ -106,6 +106,18 @@ def run_config(name, epochs):
         out[f"{mode}_epochs_per_s"] = rate
         out[f"{mode}_ms_per_epoch"] = ms
         out[f"{mode}_joseph_samples_per_s"] = 2 * S * cfg.num_gates / (ms * 1e-3)
+        # the public API with per-epoch diagnostics on (objective + rmse to the
+        # phantom every epoch; SURVEY §8d "also report a diagnostics-on number")
+        diag_epochs = max(3, min(epochs, 10))
+        cd = m.default_config(mode, norms, cfg.alpha, diag_epochs, seed=cfg.seed,
+                              stacked_norm_sq=stacked)
+        m.run(cd, problem, truth=truth)  # warm (graphs, diagnostics buffers)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        _, rec = m.run(cd, problem, truth=truth)
+        torch.cuda.synchronize()
+        out[f"{mode}_run_diagnostics_epochs_per_s"] = diag_epochs / (time.perf_counter() - t1)
+        out[f"{mode}_run_final_objective"] = rec.objective[-1]
     return out
 
 
