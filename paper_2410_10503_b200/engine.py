@@ -200,7 +200,12 @@ class Engine:
             raise ValueError("one gate sequence per slice required")
         if seqs.size and (seqs.min() < 0 or seqs.max() >= self.N):
             raise ValueError("gate index out of range")
-        self.seq = self.torch.from_numpy(seqs).to(self.device)
+        new = self.torch.from_numpy(seqs).to(self.device)
+        if self.seq is not None and tuple(self.seq.shape) == tuple(new.shape):
+            self.seq.copy_(new)  # captured epoch graphs read the sequence in place
+        else:
+            self.seq = new
+            self.graphs = {k: g for k, g in self.graphs.items() if k[0] != "spdhg"}
         self.total_iters = seqs.shape[1]
 
     def items_spdhg(self, k: int) -> _lib.Items:
@@ -258,7 +263,8 @@ class Engine:
     def epoch_graph(self, mode: str, alpha: float):
         """CUDA graph replaying one epoch (epoch counter advanced inside); one graph per
         (mode, alpha, tau, data buffer)."""
-        key = (mode, float(alpha), self.tau, self.d.data_ptr())
+        key = (mode, float(alpha), self.tau, self.d.data_ptr(),
+               self.seq.data_ptr() if mode == "spdhg" and self.seq is not None else 0)
         g = self.graphs.get(key)
         if g is None:
             torch = self.torch
@@ -290,8 +296,10 @@ class Engine:
             t.copy_(v)
 
     # ---------------------------------------------------------- diagnostics
-    def reduce(self, a, b, segments: int, length: int, mode: int):
-        out = self.torch.empty(segments, dtype=self.torch.float64, device=self.device)
+    def reduce(self, a, b, segments: int, length: int, mode: int, out=None):
+        """Fixed-order fp64 reduction of ``segments`` runs of ``length`` (into ``out``)."""
+        if out is None:
+            out = self.torch.empty(segments, dtype=self.torch.float64, device=self.device)
         _lib.check(_lib.load().mct_reduce(_lib.ptr(a), _lib.ptr(b) if b is not None else None,
                                           length, segments, length, mode, _lib.ptr(out),
                                           _lib.ptr(_lib.scratch(self.device, segments)),
@@ -309,18 +317,27 @@ class Engine:
                                                  _lib.ptr(y), _lib.ptr(out), _lib.ptr(self.ws),
                                                  _lib.stream_handle()))
 
-    def objectives(self, alpha: float, reuse_projections: bool):
-        """Per-slice objective alpha||x||^2 + sum_i ||A_i x - d_i||^2 / N (fp64)."""
+    def objective_parts(self, reuse_projections: bool, fit_out=None, xx_out=None):
+        """Device fp64 parts of the objective, no host sync: ||A_i x - d_i||^2 per
+        (slice, gate) and ||x||^2 per slice (written into ``fit_out`` / ``xx_out``)."""
         torch = self.torch
         if reuse_projections and self.proj is not None:
             proj = self.proj
         else:
-            proj = torch.empty_like(self.y)
+            if getattr(self, "_proj_scratch", None) is None:
+                self._proj_scratch = torch.empty_like(self.y)
+            proj = self._proj_scratch
             for s in range(self.S):
                 for g in range(self.N):
                     self.gated_forward(s, g, self.x[s], proj[s, g])
-        fit = self.reduce(proj, self.d, self.S * self.N, self.n_sino, _lib.REDUCE_SQDIFF)
-        xx = self.reduce(self.x, None, self.S, self.n_img, _lib.REDUCE_SQDIFF)
+        fit = self.reduce(proj, self.d, self.S * self.N, self.n_sino, _lib.REDUCE_SQDIFF,
+                          out=fit_out)
+        xx = self.reduce(self.x, None, self.S, self.n_img, _lib.REDUCE_SQDIFF, out=xx_out)
+        return fit, xx
+
+    def objectives(self, alpha: float, reuse_projections: bool):
+        """Per-slice objective alpha||x||^2 + sum_i ||A_i x - d_i||^2 / N (fp64)."""
+        fit, xx = self.objective_parts(reuse_projections)
         fit = fit.view(self.S, self.N).cpu().numpy()
         xx = xx.cpu().numpy()
         return [float(alpha * xx[s] + sum(fit[s, g] / self.N for g in range(self.N)))

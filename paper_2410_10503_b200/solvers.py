@@ -105,8 +105,20 @@ class Problem:
         return total
 
     def data_objective(self) -> float:
-        n = self.num_gates
-        return sum(fit_value(n, d, np.zeros_like(d)) for d in self.data)
+        cache = self.__dict__.setdefault("_cache", {})
+        if "data_objective" not in cache:
+            n = self.num_gates
+            cache["data_objective"] = sum(fit_value(n, d, np.zeros_like(d)) for d in self.data)
+        return cache["data_objective"]
+
+    def _engine(self, keep_projections: bool) -> Engine:
+        """The device engine run() uses for this (immutable) problem: data, warps and
+        workspace uploaded once and reused by later runs (state is reset per run)."""
+        cache = self.__dict__.setdefault("_cache", {})
+        key = ("engine", bool(keep_projections))
+        if key not in cache:
+            cache[key] = Engine([self.operators], [self.data], keep_projections=keep_projections)
+        return cache[key]
 
 
 @dataclass(frozen=True)
@@ -368,6 +380,9 @@ def step(state: SolverState, config: SolverConfig, problem: Problem,
     return state
 
 
+SYNC_EPOCHS = 32  # run(): epochs between host reads of the device diagnostics table
+
+
 def _guard(problem_data_objective: float) -> float:
     return 1e6 * max(problem_data_objective, np.finfo(np.float64).tiny)
 
@@ -391,7 +406,8 @@ def run(config: SolverConfig, problem: Problem, saddle: SaddlePoint | None = Non
         return np.zeros(problem.image_shape), record
     torch = _lib.require_cuda()
     keep = diagnostics and config.mode == "pdhg"
-    eng = state._bind(problem, keep_projections=keep)
+    eng = problem._engine(keep)  # zero state below == SolverState.zeros(problem)
+    state._engine, state._problem, state._host = eng, problem, None
     eng.set_params(config)
     eng.reset()
     n = problem.num_gates
@@ -407,6 +423,41 @@ def run(config: SolverConfig, problem: Problem, saddle: SaddlePoint | None = Non
                                         for v in saddle.y_star])).to(eng.device)
     if truth is not None:
         tr = torch.from_numpy(np.asarray(truth, dtype=np.float32)).to(eng.device)
+    # Per-epoch diagnostics are written into a device table (no host sync) and
+    # read back every SYNC_EPOCHS epochs (every epoch with an on_epoch callback).
+    # Rows are then checked in order exactly as the reference does after each
+    # epoch: the first non-finite iterate (device status words) raises first,
+    # then the objective guard, so the error message names the same epoch /
+    # iteration; nothing later than the raising epoch reaches the record.
+    cols = n + 4  # ||A_i x - d_i||^2 (n), ||x||^2, ||x - x*||^2, ||y - y*||^2, ||x - truth||^2
+    table = torch.full((config.epochs, cols), math.nan, dtype=torch.float64, device=eng.device)
+    sync_every = 1 if on_epoch is not None else SYNC_EPOCHS
+    pending = []
+
+    def flush():
+        if not pending:
+            return
+        rows = table[pending[0] - 1:pending[-1]].cpu().numpy()
+        primal, dual = eng.read_status()
+        bad = [v for v in (primal, dual[0] if dual is not None else None) if v is not None]
+        bad_epoch = (min(bad) + ipe - 1) // ipe if bad else None
+        for k, e in enumerate(pending):
+            if bad_epoch is not None and e >= bad_epoch:
+                _raise_status(eng)
+            row = rows[k]
+            objective_value = math.nan
+            if diagnostics:
+                objective_value = float(problem.alpha * row[n] + sum(row[i] / n for i in range(n)))
+                if not math.isfinite(objective_value) or objective_value > guard:
+                    raise DivergenceError(
+                        f"objective {objective_value:.3e} exceeded the divergence guard "
+                        f"at epoch {e} (iteration {e * ipe})")
+            dist = float(row[n + 1] + row[n + 2]) if xs is not None else math.nan
+            err = math.sqrt(float(row[n + 3]) / eng.n_img) if tr is not None else math.nan
+            record.append(epoch=float(e), dist_sq=dist, objective=objective_value,
+                          rmse_to_truth=err, fwd_calls=e * n, adj_calls=e * n)
+        pending.clear()
+
     for epoch_index in range(1, config.epochs + 1):
         if g is not None:
             g.replay()
@@ -418,26 +469,18 @@ def run(config: SolverConfig, problem: Problem, saddle: SaddlePoint | None = Non
         state.adj_calls += n
         if config.mode == "pdhg":
             state.last_projections = {i: None for i in range(n)}
-        if diagnostics or on_epoch is not None or epoch_index == config.epochs:
-            _raise_status(eng)
-        objective_value = math.nan
+        row = table[epoch_index - 1]
         if diagnostics:
-            objective_value = eng.objectives(problem.alpha, config.mode == "pdhg")[0]
-            if not math.isfinite(objective_value) or objective_value > guard:
-                raise DivergenceError(
-                    f"objective {objective_value:.3e} exceeded the divergence guard "
-                    f"at epoch {epoch_index} (iteration {state.iteration})")
-        dist = math.nan
+            eng.objective_parts(config.mode == "pdhg", fit_out=row[:n], xx_out=row[n:n + 1])
         if xs is not None:
-            dist = float(eng.reduce(eng.x[0], xs, 1, eng.n_img, _lib.REDUCE_SQDIFF).item())
-            dist += float(eng.reduce(eng.y[0], ys, 1, eng.N * eng.n_sino,
-                                     _lib.REDUCE_SQDIFF).item())
-        err = math.nan
+            eng.reduce(eng.x[0], xs, 1, eng.n_img, _lib.REDUCE_SQDIFF, out=row[n + 1:n + 2])
+            eng.reduce(eng.y[0], ys, 1, eng.N * eng.n_sino, _lib.REDUCE_SQDIFF,
+                       out=row[n + 2:n + 3])
         if tr is not None:
-            err = math.sqrt(float(eng.reduce(eng.x[0], tr, 1, eng.n_img,
-                                             _lib.REDUCE_SQDIFF).item()) / eng.n_img)
-        record.append(epoch=float(epoch_index), dist_sq=dist, objective=objective_value,
-                      rmse_to_truth=err, fwd_calls=state.fwd_calls, adj_calls=state.adj_calls)
+            eng.reduce(eng.x[0], tr, 1, eng.n_img, _lib.REDUCE_SQDIFF, out=row[n + 3:n + 4])
+        pending.append(epoch_index)
+        if len(pending) >= sync_every or epoch_index == config.epochs:
+            flush()
         if on_epoch is not None:
             on_epoch(epoch_index, state)
     return state.x, record

@@ -188,6 +188,32 @@ def solver_c1():
     np.savez_compressed(HERE / "solver_c1.npz", **out)
 
 
+def divergence_cases():
+    """The reference's DivergenceError messages on the tiny preset with
+    inadmissible (understated-norm) step sizes (solvers.py:401-419)."""
+    import json
+
+    from mctomo.solvers import DivergenceError
+
+    with np.load(HERE / "solver_tiny.npz") as f:
+        G = {k: f[k] for k in f.files}
+    r, c, a, b, sp = G["geom"]
+    geom = Geometry(int(r), int(c), int(a), int(b), float(sp))
+    motion = [MotionParams("rigid", float(p[0]), (float(p[1]), float(p[2]))) for p in G["motion"]]
+    prob = Problem.from_parts(float(G["alpha"]), gate_operators(geom, motion, True),
+                              list(G["data"]))
+    out = []
+    for mode, scale in (("pdhg", 1000.0), ("spdhg", 1000.0), ("pdhg", 30.0)):
+        cfg = default_config(mode, np.asarray(G["gate_norms"]) / scale, prob.alpha, 200, seed=3)
+        try:
+            run(cfg, prob)
+            msg = None
+        except DivergenceError as exc:
+            msg = str(exc)
+        out.append({"mode": mode, "norm_scale": scale, "seed": 3, "epochs": 200, "message": msg})
+    (HERE / "divergence.json").write_text(json.dumps(out, indent=1) + "\n")
+
+
 def dataset_cases():
     """Data generation + file formats (§8f #3/#4): phantoms, the pinned noise
     stream, generate(), and the reference's own on-disk files (dataset and
@@ -250,9 +276,11 @@ def dataset_cases():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["projector", "warps", "sampling", "tiny", "c1", "datasets"]
+    which = sys.argv[1:] or ["projector", "warps", "sampling", "tiny", "c1", "datasets",
+                             "divergence"]
     for w in which:
         t0 = time.time()
         {"projector": projector_cases, "warps": warp_cases, "sampling": sampling_cases,
-         "tiny": solver_tiny, "c1": solver_c1, "datasets": dataset_cases}[w]()
+         "tiny": solver_tiny, "c1": solver_c1, "datasets": dataset_cases,
+         "divergence": divergence_cases}[w]()
         print(f"{w}: {time.time() - t0:.1f}s", flush=True)

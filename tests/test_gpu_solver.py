@@ -163,6 +163,62 @@ def test_divergence_guard_fires(m, golden_tiny):
         m.run(cfg, problem)
 
 
+@pytest.mark.parametrize("case", range(3))
+def test_divergence_message_matches_reference(m, golden_tiny, case):
+    """Same epoch / iteration in the DivergenceError as the reference
+    (golden/divergence.json), with the deferred diagnostics table and with a
+    per-epoch callback (host sync every epoch)."""
+    import json
+    import re
+
+    from conftest import GOLDEN
+
+    ref = json.loads((GOLDEN / "divergence.json").read_text())[case]
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    cfg = m.default_config(ref["mode"], np.asarray(G["gate_norms"]) / ref["norm_scale"],
+                           problem.alpha, ref["epochs"], seed=ref["seed"])
+    where = re.search(r"at epoch \d+ \(iteration \d+\)", ref["message"]).group(0)
+    for cb in (None, lambda e, st: None):
+        with pytest.raises(m.DivergenceError, match=re.escape(where)):
+            m.run(cfg, problem, on_epoch=cb)
+
+
+def test_engine_reuse_across_runs(m, golden_tiny):
+    """run() keeps one device engine per problem; new seeds / step sizes / modes
+    on the same problem give exactly what a fresh problem gives."""
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    a = tiny_config(m, G, "spdhg", 5, epochs=6)
+    b = tiny_config(m, G, "spdhg", 11, epochs=6)
+    p = tiny_config(m, G, "pdhg", 0, epochs=6)
+    xa, _ = m.run(a, problem)
+    xb, _ = m.run(b, problem)
+    xp, _ = m.run(p, problem)
+    xa2, _ = m.run(a, problem)
+    assert np.array_equal(xa, xa2) and not np.array_equal(xa, xb)
+    for cfg, x in ((b, xb), (p, xp)):
+        xf, _ = m.run(cfg, tiny_problem(m, G))
+        assert np.array_equal(x, xf)
+
+
+def test_deferred_diagnostics_equal_per_epoch(m, golden_tiny):
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    cfg = tiny_config(m, G, "spdhg", 5, epochs=40)
+    saddle = m.SaddlePoint(x_star=np.ones(problem.image_shape),
+                           y_star=[np.zeros(d.shape) for d in problem.data], source="test",
+                           converged=True, residual=0.0)
+    truth = np.full(problem.image_shape, 0.5)
+    x1, r1 = m.run(cfg, problem, saddle=saddle, truth=truth)
+    seen = []
+    x2, r2 = m.run(cfg, problem, saddle=saddle, truth=truth,
+                   on_epoch=lambda e, st: seen.append(e))
+    assert np.array_equal(x1, x2) and seen == list(range(1, 41))
+    for col in ("epochs", "dist_sq", "objective", "rmse_to_truth", "fwd_calls", "adj_calls"):
+        assert getattr(r1, col) == getattr(r2, col), col
+
+
 def test_run_batch_equals_single_runs(m):
     from paper_2410_10503_b200 import workloads
 
