@@ -131,6 +131,14 @@ int mct_gated_forward(const mct_family* fam, int slice, int gate, const float* x
 int mct_gated_adjoint(const mct_family* fam, int slice, int gate, const float* y_dev,
                       float* img_dev, void* workspace_dev, void* stream);
 
+/* The gated forwards of `count` gates of one slice in one pass (two launches):
+ * sino_dev[k] = A(D_{gates_dev[k]} x), sino_dev (count, A, B).  The objective of
+ * solvers._epoch_objective / Problem.objective (solvers.py:113-119, :422-432)
+ * needs every gate's projection; the workspace must hold `count` items.        */
+int mct_gated_forward_many(const mct_family* fam, int slice, const int32_t* gates_dev, int count,
+                           const float* x_dev, float* sino_dev, void* workspace_dev,
+                           void* stream);
+
 /* ------------------------------------------------------------------------- */
 /* Fused solver iteration (solvers.step, solvers.py:316-366).
  *

@@ -97,6 +97,8 @@ SIGNATURES = {
     "mct_dot_f64": (c_int, [c_void_p, c_void_p, c_longlong, c_void_p, c_void_p, c_void_p]),
     "mct_gaussian_field": (c_int, [c_uint64, c_uint64, c_longlong, c_double, c_void_p, c_void_p,
                                    c_int, c_void_p]),
+    "mct_gated_forward_many": (c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_void_p,
+                                       c_void_p, c_void_p]),
     "mct_exchange_post": (c_int, [c_void_p, c_int, c_int, c_uint64, c_void_p]),
     "mct_exchange_z_update": (c_int, [c_void_p, c_void_p, c_int, c_uint64, c_longlong, c_void_p,
                                       c_void_p, c_double, c_void_p, c_void_p]),

@@ -569,6 +569,33 @@ int mct_gated_forward(const mct_family* fam, int slice, int gate, const float* x
     return MCT_OK;
 }
 
+int mct_gated_forward_many(const mct_family* fam, int slice, const int32_t* gates, int count,
+                           const float* x, float* sino, void* ws, void* stream) {
+    MCT_REQUIRE(fam && gates && x && sino && ws, "null argument");
+    MCT_REQUIRE(slice >= 0 && slice < fam->S, "slice out of range");
+    MCT_REQUIRE(count >= 1 && count <= fam->N, "count must lie in [1, num_gates]");
+    const mct_ray_plan* rp = fam->ray;
+    cudaStream_t st = (cudaStream_t)stream;
+    ItemSel sel;
+    memset(&sel, 0, sizeof(sel));
+    sel.gates = gates;  // item k -> gates[k] of this slice
+    sel.ips = count;
+    sel.num_slices = 1;
+    PackArgs pa = pack_args(rp, ws);
+    pa.sel = sel;
+    pa.N = fam->N;
+    pa.x = x;
+    pa.warps = fam->d_warps + (size_t)slice * fam->N;
+    MCT_CUDA(launch_pack(pa, count, st), "gated pack (many)");
+    FwdArgs fa = fwd_args(rp, ws);
+    fa.sel = sel;
+    fa.ksplit = count > 1 ? 1 : rp->ksplit1;  // as the fused iteration (see MCT_KSPLIT_MIN)
+    fa.out = sino;
+    fa.out_item_stride = (long long)rp->A * rp->B;
+    MCT_CUDA(launch_fwd(fa, 0, count, st), "gated forward (many)");
+    return MCT_OK;
+}
+
 int mct_gated_adjoint(const mct_family* fam, int slice, int gate, const float* y, float* img,
                       void* ws, void* stream) {
     MCT_REQUIRE(fam && y && img && ws, "null argument");

@@ -327,9 +327,16 @@ class Engine:
             if getattr(self, "_proj_scratch", None) is None:
                 self._proj_scratch = torch.empty_like(self.y)
             proj = self._proj_scratch
-            for s in range(self.S):
-                for g in range(self.N):
-                    self.gated_forward(s, g, self.x[s], proj[s, g])
+            if self.max_items >= self.N:  # all gates of a slice in one pass
+                for s in range(self.S):
+                    _lib.check(_lib.load().mct_gated_forward_many(
+                        self.family.handle, s, _lib.ptr(self.all_gates), self.N,
+                        _lib.ptr(self.x[s]), _lib.ptr(proj[s]), _lib.ptr(self.ws),
+                        _lib.stream_handle()))
+            else:
+                for s in range(self.S):
+                    for g in range(self.N):
+                        self.gated_forward(s, g, self.x[s], proj[s, g])
         fit = self.reduce(proj, self.d, self.S * self.N, self.n_sino, _lib.REDUCE_SQDIFF,
                           out=fit_out)
         xx = self.reduce(self.x, None, self.S, self.n_img, _lib.REDUCE_SQDIFF, out=xx_out)

@@ -339,3 +339,27 @@ def test_helper_maps_on_device(m, rng):
     # ||stack||^2 == lambda_max(sum_i A_i^* A_i)  (linops.py:275-289)
     nsq = m.power_method(st, iterations=60) ** 2
     assert nsq == pytest.approx(m.stacked_norm_sq(ops, iterations=60), rel=1e-4)
+
+
+def test_gated_forward_many_matches_single(m, rng):
+    """mct_gated_forward_many (all gates of a slice in one pass, used by the
+    per-epoch objective) vs one gated forward per gate."""
+    import torch
+
+    from paper_2410_10503_b200 import _lib
+    from paper_2410_10503_b200.engine import Engine
+
+    geom = m.Geometry(40, 36, 30, 57, 1.0)
+    gates = [m.MotionParams.identity(), m.MotionParams(kind="rigid", rotation=0.3),
+             rng.uniform(-2, 2, (2, 40, 36)).astype(np.float32)]
+    ops = m.gate_operators(geom, gates)
+    data = [np.zeros(geom.sino_shape) for _ in ops]
+    eng = Engine([ops], [data])
+    x = torch.from_numpy(rng.standard_normal(geom.image_shape).astype(np.float32)).cuda()
+    out = torch.empty((3,) + tuple(geom.sino_shape), device="cuda")
+    _lib.check(_lib.load().mct_gated_forward_many(eng.family.handle, 0, _lib.ptr(eng.all_gates),
+                                                  3, _lib.ptr(x), _lib.ptr(out), _lib.ptr(eng.ws),
+                                                  _lib.stream_handle()))
+    for k, op in enumerate(ops):
+        ref = op.apply_device(x)
+        assert rel_l2(out[k].double().cpu().numpy(), ref.double().cpu().numpy()) <= 1e-6

@@ -108,7 +108,7 @@ def run_config(name, epochs):
         out[f"{mode}_joseph_samples_per_s"] = 2 * S * cfg.num_gates / (ms * 1e-3)
         # the public API with per-epoch diagnostics on (objective + rmse to the
         # phantom every epoch; SURVEY §8d "also report a diagnostics-on number")
-        diag_epochs = 200 if name in ("c1", "c2") else 20  # includes run()'s own setup
+        diag_epochs = 200 if name in ("c1", "c2") else 50  # includes run()'s own setup
         cd = m.default_config(mode, norms, cfg.alpha, diag_epochs, seed=cfg.seed,
                               stacked_norm_sq=stacked)
         m.run(cd, problem, truth=truth)  # warm (graphs, diagnostics buffers)
