@@ -41,6 +41,7 @@ struct AdjAngle {
 // A^* splits its angle loop over up to MCT_MAX_ASPLIT blocks per tile when one
 // launch has too few tiles to fill 148 SMs (single-gate SPDHG); each split
 // writes its own partial image slot and K4 sums the slots in a fixed order.
+// The item workspace holds as many slots as the plan's single-item split.
 #ifndef MCT_MAX_ASPLIT
 #define MCT_MAX_ASPLIT 16
 #endif
