@@ -350,6 +350,9 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(Fw
 #ifndef ADJ_MIN_BLOCKS
 #define ADJ_MIN_BLOCKS 10
 #endif
+#ifndef ADJ_SPLIT_RULE
+#define ADJ_SPLIT_RULE 1
+#endif
 #define INV_2_32 2.3283064365386963e-10f
 
 // Tent weights of bins floor(jc) .. for a pixel whose jc has fraction tlo/2^32,
@@ -573,9 +576,9 @@ cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-// Angle split of A^*: fill one wave of resident blocks when a launch has few
-// tiles (single-gate SPDHG), never exceeding it (a partial second wave would
-// idle most SMs); every split keeps >= 16 angles.
+// Angle split of A^* for launches with fewer tiles than resident blocks
+// (single-gate SPDHG): chosen by a wave-quantisation cost model (below); every
+// split keeps >= MCT_ASPLIT_MIN_PAIRS angle pairs.
 static inline int adj_tiles_x(int cols) { return ((cols + 1) / 2 + ADJ_TW - 1) / ADJ_TW; }
 
 int choose_asplit(const mct_ray_plan* rp, int items) {
@@ -591,13 +594,33 @@ int choose_asplit(const mct_ray_plan* rp, int items) {
     }
     const long long tiles = (long long)adj_tiles_x(rp->cols) * ((rp->rows + ADJ_TH - 1) / ADJ_TH) *
                             (items > 0 ? items : 1);
-    long long s = tiles >= slots ? 1 : slots / tiles;
-    s = s < 1 ? 1 : s;
-    s = s > MCT_MAX_ASPLIT ? MCT_MAX_ASPLIT : s;
     // >= MCT_ASPLIT_MIN_PAIRS angle pairs per split
     const long long by_angles =
         rp->A / (2 * MCT_ASPLIT_MIN_PAIRS) > 0 ? rp->A / (2 * MCT_ASPLIT_MIN_PAIRS) : 1;
-    return (int)(s < by_angles ? s : by_angles);
+    const long long smax = by_angles < MCT_MAX_ASPLIT ? by_angles : MCT_MAX_ASPLIT;
+#if ADJ_SPLIT_RULE == 0
+    long long s = tiles >= slots ? 1 : slots / tiles;  // fill at most one wave
+    s = s < 1 ? 1 : s;
+    return (int)(s < smax ? s : smax);
+#else
+    // launches of a wave or more already balance dynamically: no split (every
+    // extra slot costs K4 one more partial-image read per gather)
+    if (tiles >= slots) return 1;
+    // fewer tiles than resident blocks: the split minimising (waves, rounded up)
+    // x (angle pairs per block), e.g. C3 single gate: 11 splits in 1.9 waves
+    // beat 5 splits in one 86 %-full wave
+    const long long P = rp->A > 2 ? (rp->A - 1) / 2 : 1;
+    long long best = 1, best_cost = -1;
+    for (long long s = 1; s <= smax; ++s) {
+        const long long waves = (tiles * s + slots - 1) / slots;
+        const long long cost = waves * ((P + s - 1) / s);
+        if (best_cost < 0 || cost * 100 < best_cost * 97) {  // >= 3 % better to split more
+            best = s;
+            best_cost = cost;
+        }
+    }
+    return (int)best;
+#endif
 }
 
 cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, cudaStream_t st) {
