@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(const float* __restrict__ a
     const float* as = a + (long long)s * stride;
     const float* bs = b ? b + (long long)s * stride : nullptr;
     double acc = 0.0;
+#pragma unroll 4
     for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         const double x = (double)__ldg(as + i);
         if (mode == MCT_REDUCE_DOT) {
@@ -241,17 +242,22 @@ __global__ void axpby_mixed_kernel(long long n, double alpha, const void* __rest
     }
 }
 
+// max |x| over the grid: block maxima combined with an integer atomicMax on the
+// bit patterns (order-preserving for non-negative floats; max is order-free, so
+// the result is deterministic).  *out must be zeroed first.
 __global__ void absmax_kernel(const float* __restrict__ x, long long n, float* out) {
     __shared__ float sh[256];
     float m = 0.0f;
-    for (long long i = threadIdx.x; i < n; i += blockDim.x) m = fmaxf(m, fabsf(x[i]));
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        m = fmaxf(m, fabsf(x[i]));
     sh[threadIdx.x] = m;
     __syncthreads();
     for (int w = 128; w > 0; w >>= 1) {
         if (threadIdx.x < w) sh[threadIdx.x] = fmaxf(sh[threadIdx.x], sh[threadIdx.x + w]);
         __syncthreads();
     }
-    if (threadIdx.x == 0) *out = sh[0];
+    if (threadIdx.x == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(sh[0]));
 }
 
 inline int grid_for(long long n, int block) {
@@ -293,7 +299,7 @@ cudaError_t launch_warp_fwd_plain(const WarpDesc* d_desc, const float* x, float*
 }
 
 static int reduce_parts(long long len) {
-    long long p = (len + 8191) / 8192;  // >= 8K elements per block
+    long long p = (len + 2047) / 2048;  // >= 2K elements per block
     return (int)(p < 1 ? 1 : (p > MCT_REDUCE_PARTS ? MCT_REDUCE_PARTS : p));
 }
 
@@ -334,7 +340,9 @@ cudaError_t launch_dot_f64(const double* a, const double* b, long long n, double
 }
 
 cudaError_t launch_absmax(const float* x, long long n, float* out, cudaStream_t st) {
-    absmax_kernel<<<1, 256, 0, st>>>(x, n, out);
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(float), st);
+    if (e != cudaSuccess) return e;
+    absmax_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, out);
     return cudaGetLastError();
 }
 
