@@ -75,7 +75,9 @@ struct mct_ray_plan {
 #ifndef MCT_KSPLIT_MAX
 #define MCT_KSPLIT_MAX 4
 #endif
+#ifndef MCT_FWD_ANGLES
 #define MCT_FWD_ANGLES 4
+#endif
 
 // --------------------------------------------------------------- warp plan --
 struct WarpDesc {

@@ -346,7 +346,9 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(Fw
 #endif
 #define ADJ_TH (ADJ_PPT * ADJ_WARPS)
 #define ADJ_THREADS (ADJ_TW * ADJ_WARPS)
+#ifndef ADJ_CH
 #define ADJ_CH ADJ_THREADS
+#endif
 #ifndef ADJ_MIN_BLOCKS
 #define ADJ_MIN_BLOCKS 10
 #endif
