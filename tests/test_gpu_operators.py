@@ -285,6 +285,11 @@ def test_dense_gated_parity_full_size(m, n, peak):
     (50, 20, 13, 9, 2.5),       # detector narrower than the image (rays miss corners)
     (32, 32, 7, 200, 0.3),      # fine bins: wide adjoint footprint (K = 3)
     (19, 41, 64, 61, 1.0),      # non-square, 45-degree tie handled by the host flags
+    (1, 40, 6, 45, 1.0),        # one-row image
+    (40, 1, 6, 45, 1.0),        # one-column image (centre column = its own mirror)
+    (33, 33, 2, 47, 1.0),       # two angles: 0 and pi/2 only, no mirror pairs
+    (33, 35, 3, 47, 1.0),       # odd angle count: one mirror pair + angle 0
+    (64, 64, 200, 91, 1.0),     # the reference's default angle count (45 deg is cols-dominant)
 ])
 def test_edge_geometries_vs_oracle(m, g):
     r = np.random.default_rng(sum(int(v) for v in g[:4]))
