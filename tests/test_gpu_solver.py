@@ -307,6 +307,26 @@ def test_c2_shape_spdhg_trajectory_vs_oracle(m):
     assert rel_l2(x, st.x) <= ITER_TOL
 
 
+def test_c3_pdhg_epoch_vs_oracle(m):
+    """BASELINE C3 at full size (512^2, 20 dense gates, 720x729): one PDHG epoch of
+    the bench workload vs the fp64 oracle, identical step sizes."""
+    from paper_2410_10503_b200 import workloads
+
+    cfgw = workloads.CONFIGS["c3"]
+    problem, truth, inp = m.simulate.workload_problem(cfgw, 0)
+    norm = float(np.sqrt(0.966 * cfgw.num_angles * cfgw.n))  # SURVEY §8d estimate
+    cfg = m.default_config("pdhg", [norm] * cfgw.num_gates, cfgw.alpha, 1,
+                           stacked_norm_sq=cfgw.num_gates * norm ** 2)
+    x, rec = m.run(cfg, problem)
+    oops = oracle.gate_operators(oracle.Geometry(*cfgw.geometry_args), inp.gates,
+                                 threads=oracle.default_threads())
+    ocfg = osolver.default_config("pdhg", [norm] * cfgw.num_gates, cfgw.alpha, 1,
+                                  stacked_norm_sq=cfgw.num_gates * norm ** 2)
+    st, objs = osolver.run(ocfg, cfgw.alpha, oops, [np.asarray(d) for d in problem.data])
+    assert rel_l2(x, st.x) <= ITER_TOL
+    assert rec.objective[0] == pytest.approx(objs[0], rel=ITER_TOL)
+
+
 def test_cg_reference_matches_reference_saddle(m, golden_tiny):
     """Device CG saddle (solvers.py:435-490) vs the reference's fp64 CG saddle."""
     G = golden_tiny
