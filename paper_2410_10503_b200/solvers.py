@@ -113,9 +113,13 @@ class Problem:
 
     def _engine(self, keep_projections: bool) -> Engine:
         """The device engine run() uses for this (immutable) problem: data, warps and
-        workspace uploaded once and reused by later runs (state is reset per run)."""
+        workspace uploaded once and reused by later runs (state is reset per run).
+        One engine per (device, stream), so runs issued concurrently on different
+        streams never share state."""
+        torch = _lib.require_cuda()
         cache = self.__dict__.setdefault("_cache", {})
-        key = ("engine", bool(keep_projections))
+        stream = torch.cuda.current_stream()
+        key = ("engine", bool(keep_projections), stream.device.index, stream.cuda_stream)
         if key not in cache:
             cache[key] = Engine([self.operators], [self.data], keep_projections=keep_projections)
         return cache[key]
