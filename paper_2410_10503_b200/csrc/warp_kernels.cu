@@ -10,24 +10,34 @@
 
 namespace {
 
+#ifndef K4_LANES
+#define K4_LANES 4
+#endif
 // K4 — one thread per pixel q of one slice (blockIdx.y): sums D_g^* img_k over
 // the slice's items in a fixed order (deterministic), then
 //   mode 0: out = sum                       (standalone D^* / gated adjoint)
 //   mode 1: z += sum; zbar = z + sum_k (theta/p_k) D^*img_k; x = x_next
 //   mode 2: dz = sum; x = x_next            (gate-sharded PDHG partial)
-template <int MODE>
+// LANES > 1 (multi-gate launches): a block is 32 pixels x LANES gate lanes;
+// lane l sums gates l, l+LANES, ... in order, then lane 0 adds the LANES partial
+// sums in lane order (fixed association: deterministic), so the per-pixel gate
+// chains run LANES-wide in parallel instead of one after the other.
+template <int MODE, int LANES>
 __global__ void __launch_bounds__(256) update_kernel(UpdArgs p) {
     const int slice = blockIdx.y;
     const long long n = (long long)p.rows * p.cols;
-    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= n) return;
-    const int qr = (int)(q / p.cols), qc = (int)(q - (long long)qr * p.cols);
-    const long long o = (long long)slice * n + q;
+    const int lane = LANES > 1 ? (int)threadIdx.y : 0;
+    const long long q = (long long)blockIdx.x * (LANES > 1 ? 32 : blockDim.x) + threadIdx.x;
+    if (LANES == 1 && q >= n) return;
+    const bool valid = q < n;
+    const long long qv = valid ? q : n - 1;
+    const int qr = (int)(qv / p.cols), qc = (int)(qv - (long long)qr * p.cols);
+    const long long o = (long long)slice * n + qv;
     // state loads issued ahead of the gather's dependent chain
-    const float z0 = MODE == 1 ? p.z[o] : 0.0f;
-    const float xn = MODE != 0 ? __ldg(p.x_next + o) : 0.0f;
+    const float z0 = MODE == 1 && lane == 0 ? p.z[o] : 0.0f;
+    const float xn = MODE != 0 && lane == 0 ? __ldg(p.x_next + o) : 0.0f;
     float sum = 0.0f, wsum = 0.0f;
-    for (int k = 0; k < p.sel.ips; ++k) {
+    for (int k = lane; k < p.sel.ips; k += LANES) {
         const int item = slice * p.sel.ips + k;
         int s_, gate, iter;
         resolve_item(p.sel, item, s_, gate, iter);
@@ -61,6 +71,18 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs p) {
         }
         sum += v;
         if (MODE == 1) wsum = fmaf(p.gp[gate].theta_over_p, v, wsum);
+    }
+    if (LANES > 1) {
+        __shared__ float s_sum[LANES][32], s_w[LANES][32];
+        s_sum[lane][threadIdx.x] = sum;
+        s_w[lane][threadIdx.x] = wsum;
+        __syncthreads();
+        if (lane != 0 || !valid) return;
+#pragma unroll
+        for (int l = 1; l < LANES; ++l) {
+            sum += s_sum[l][threadIdx.x];
+            wsum += s_w[l][threadIdx.x];
+        }
     }
     if (MODE == 0) {
         p.out[o] = sum;
@@ -270,11 +292,21 @@ inline int grid_for(long long n, int block) {
 
 cudaError_t launch_update(const UpdArgs& a, int mode, int slices, cudaStream_t st) {
     const long long n = (long long)a.rows * a.cols;
+    if (a.sel.ips >= K4_LANES && K4_LANES > 1) {  // several gates per slice: gate lanes
+        dim3 block(32, K4_LANES), grid((unsigned)((n + 31) / 32), slices);
+        switch (mode) {
+            case 0: update_kernel<0, K4_LANES><<<grid, block, 0, st>>>(a); break;
+            case 1: update_kernel<1, K4_LANES><<<grid, block, 0, st>>>(a); break;
+            case 2: update_kernel<2, K4_LANES><<<grid, block, 0, st>>>(a); break;
+            default: return cudaErrorInvalidValue;
+        }
+        return cudaGetLastError();
+    }
     dim3 block(256), grid((unsigned)((n + 255) / 256), slices);
     switch (mode) {
-        case 0: update_kernel<0><<<grid, block, 0, st>>>(a); break;
-        case 1: update_kernel<1><<<grid, block, 0, st>>>(a); break;
-        case 2: update_kernel<2><<<grid, block, 0, st>>>(a); break;
+        case 0: update_kernel<0, 1><<<grid, block, 0, st>>>(a); break;
+        case 1: update_kernel<1, 1><<<grid, block, 0, st>>>(a); break;
+        case 2: update_kernel<2, 1><<<grid, block, 0, st>>>(a); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
