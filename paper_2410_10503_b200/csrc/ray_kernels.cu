@@ -21,8 +21,8 @@ namespace {
 // one halo element per thread, so the warp's dependent load chain is paid once
 // per thread on a small grid.  Same per-element arithmetic (bitwise equal).
 // ---------------------------------------------------------------------------
-template <int T, int THREADS>
-__global__ void __launch_bounds__(THREADS) pack_kernel(PackArgs p) {
+template <int T, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) pack_kernel(PackArgs p) {
     constexpr int H = T + 1;
     __shared__ float tile[H][H + 1];
     const int item = blockIdx.z;
@@ -528,13 +528,19 @@ __global__ void __launch_bounds__(ADJ_THREADS, ADJ_MIN_BLOCKS) adj_kernel(AdjArg
 
 }  // namespace
 
+#ifndef PACK_SMALL_ITEMS
+#define PACK_SMALL_ITEMS 1
+#endif
+#ifndef PACK32_MINB
+#define PACK32_MINB 6
+#endif
 cudaError_t launch_pack(const PackArgs& a, int items, cudaStream_t st) {
-    if (items == 1) {  // single gate: small tiles, one halo element per thread
+    if (items <= PACK_SMALL_ITEMS) {  // few gates: small tiles, one halo element per thread
         dim3 grid((a.cols + 15) / 16, (a.rows + 15) / 16, items);
-        pack_kernel<16, 320><<<grid, 320, 0, st>>>(a);
+        pack_kernel<16, 320, 1><<<grid, 320, 0, st>>>(a);
     } else {
         dim3 grid((a.cols + 31) / 32, (a.rows + 31) / 32, items);
-        pack_kernel<32, 256><<<grid, 256, 0, st>>>(a);
+        pack_kernel<32, 256, PACK32_MINB><<<grid, 256, 0, st>>>(a);
     }
     return cudaGetLastError();
 }
