@@ -139,6 +139,9 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
     asm("sub.cc.u32 %0, %0, %2;\n\tsubc.u32 %1, %1, %3;" : "+r"(lo), "+r"(hi) : "r"(ilo), "r"(ihi));
 }
 
+#ifndef FWD_ACQREL
+#define FWD_ACQREL 1
+#endif
 #define FWD_ANGLES MCT_FWD_ANGLES  // warps (= consecutive angles) per block; they share L1 lines
 #ifndef FWD_MIN_BLOCKS
 #define FWD_MIN_BLOCKS 12         // 12 x 4 warps resident: 40 registers for 8 loads in flight
@@ -278,16 +281,26 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(Fw
         __shared__ int s_last;
         __syncthreads();
         if (threadIdx.x == 0 && threadIdx.y == 0) {
-            __threadfence();
             int* cnt = reinterpret_cast<int*>(const_cast<char*>(base) + p.off_cnt) +
                        blockIdx.y * gridDim.x + blockIdx.x;
+#if FWD_ACQREL
+            // release: the block's PART stores (ordered before by the barrier);
+            // acquire: the other parts' stores, for the last block to arrive
+            int prev;
+            asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                         : "=r"(prev) : "l"(cnt) : "memory");
+#else
+            __threadfence();
             const int prev = atomicAdd(cnt, 1);
+#endif
             s_last = (prev == ks - 1);
             if (s_last) *cnt = 0;  // every part has arrived: re-arm for the next launch
         }
         __syncthreads();
         if (!s_last || !active) return;
+#if !FWD_ACQREL
         __threadfence();
+#endif
         sum = 0.0;
         for (int q = 0; q < ks; ++q) sum += __ldcg(PART + ((long long)q * p.A + a) * p.B + j);
     } else if (!active) {
