@@ -587,7 +587,24 @@ int choose_ksplit(int A, int B, int n) {
     return (int)k;
 }
 
+// K2 lives on its L1 hit rate (the four angles of a block re-read the same lines
+// while their warps drift apart by a few rows): ask for the smallest shared-memory
+// carve-out that still fits the resident blocks, i.e. the largest L1.
+static void fwd_prefer_l1() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+#ifdef FWD_CARVEOUT_PCT
+    const int pct = FWD_CARVEOUT_PCT;
+#else
+    const int pct = 7;  // >= 12 blocks x 1 KB reserved of 228 KB -> the 16 KB config
+#endif
+    cudaFuncSetAttribute(fwd_kernel<0>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel<1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st) {
+    fwd_prefer_l1();
     dim3 block(32, FWD_ANGLES),
         grid((a.B + 31) / 32, (a.A + FWD_ANGLES - 1) / FWD_ANGLES, items * a.ksplit);
     if (mode == 0)
