@@ -6,6 +6,7 @@ python bench.py --config c5 --steps 10 --warmup 3 > gpurun_out/bench_c5.json 2> 
 python bench.py --config c4 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
 python tools/bench_configs.py --out gpurun_out/configs.json > gpurun_out/configs.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1
+ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_timed.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_timed.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"fwd_kernel|adj_kernel|pack_kernel|update_kernel" -s 4 -c 4 -o gpurun_out/prof_c3_pdhg_final python tools/prof_iter.py --config c3 --mode pdhg --iters 3 > gpurun_out/ncu_pdhg.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"fwd_kernel|adj_kernel|pack_kernel|update_kernel" -s 40 -c 4 -o gpurun_out/prof_c3_spdhg_final python tools/prof_iter.py --config c3 --mode spdhg --iters 20 > gpurun_out/ncu_spdhg.log 2>&1
 ls -la gpurun_out/
