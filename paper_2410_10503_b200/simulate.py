@@ -27,7 +27,7 @@ import numpy as np
 
 from . import _lib
 from .linops import LinearMap, compose, power_method, stacked_norm_sq
-from .motion import DenseWarpOperator, MotionParams, WarpOperator, motion_sequence, warp_from_spec
+from .motion import DenseWarpOperator, MotionParams, motion_sequence, warp_from_spec
 from .projector import Geometry, ray_transform
 from .workloads import _grids, gaussian_field, noisy_data
 

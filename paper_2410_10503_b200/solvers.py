@@ -24,14 +24,14 @@ and ``distributed.run_pdhg_sharded`` (PDHG gate-sharded over GPUs).
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Callable, Sequence
 
 import numpy as np
 
 from . import _lib
 from .engine import Engine
-from .experiment_io import ConvergenceRecord, rmse
+from .experiment_io import ConvergenceRecord
 from .functionals import fit_value, g_value, moduli
 from .linops import LinearMap
 
