@@ -350,6 +350,14 @@ def run_ours(args, cfg):
     launches_per_step = (7 if exchange == "p2p" else 6) if use_dist else 5
     for _ in range(args.warmup):
         step_fn()
+    if use_dist and exchange == "p2p" and worker.p2p_failed_anywhere():
+        # a peer wait timed out on some rank during warm-up: every rank switches
+        print(json.dumps({"warning": "p2p exchange timed out in warm-up; using nccl"}),
+              file=sys.stderr)
+        worker.fallback_to_nccl()
+        exchange = "nccl"
+        for _ in range(args.warmup):
+            step_fn()
     hbm_peak, peak_src = peaks()
     step_events = [[torch.cuda.Event(enable_timing=True) for _ in range(5)]
                    for _ in range(args.steps)]

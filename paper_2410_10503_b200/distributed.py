@@ -198,6 +198,25 @@ class ShardedPDHG:
         if self.p2p:
             self.p2p.check()
 
+    def p2p_failed_anywhere(self, group=None) -> bool:
+        """True when any rank's p2p exchange timed out (collective over the group)."""
+        import torch.distributed as dist
+
+        flag = self.engine.torch.zeros(1, dtype=self.engine.torch.int32,
+                                       device=self.engine.device)
+        if self.p2p is not None:
+            flag.copy_(self.p2p.failed)
+        if dist.is_available() and dist.is_initialized():
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+        return bool(int(flag.item()))
+
+    def fallback_to_nccl(self):
+        """Switch this worker to the NCCL exchange and restart from the zero state."""
+        self.p2p = None
+        self.exchange = "nccl"
+        self.dz = self.engine.torch.zeros_like(self.engine.x)
+        self.engine.reset()
+
 
 def run_pdhg_sharded(config, problem, group=None, exchange: str = "nccl"):
     """PDHG over the ranks of ``group``; returns x (float64 numpy) on every rank.
