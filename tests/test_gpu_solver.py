@@ -286,6 +286,13 @@ def test_p2p_exchange_matches_nccl_single_rank(m, golden_tiny):
         torch.cuda.synchronize()
         pad = w.p2p.buf[-256:].view(torch.int64)[0].item()
         assert pad == 3 and w.p2p.epoch == 3 and int(w.p2p.failed.item()) == 0
+        assert not w.p2p_failed_anywhere()
+        w.p2p.failed.fill_(1)  # as if a peer wait had timed out
+        assert w.p2p_failed_anywhere()
+        w.fallback_to_nccl()
+        for _ in range(cfg.epochs):
+            w.finish(w.local_iteration())
+        assert np.array_equal(w.engine.x[0].double().cpu().numpy(), x_nccl)
     finally:
         dist.destroy_process_group()
 
