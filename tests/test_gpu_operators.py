@@ -368,3 +368,41 @@ def test_gated_forward_many_matches_single(m, rng):
     for k, op in enumerate(ops):
         ref = op.apply_device(x)
         assert rel_l2(out[k].double().cpu().numpy(), ref.double().cpu().numpy()) <= 1e-6
+
+
+@pytest.mark.parametrize("g", [(1, 1, 1, 1, 1.0), (7, 3, 5, 4, 0.8), (40, 1, 6, 45, 1.0),
+                               (32, 32, 7, 200, 0.3), (65, 66, 48, 95, 1.0)])
+def test_no_writes_outside_buffers(m, g):
+    """Out-of-bounds write check without a sanitizer: workspace and outputs carry
+    canary tails (0xAB) that every launch must leave intact, and a second
+    forward / adjoint on the reused workspace reproduces the first bit for bit
+    (the zero pads survived)."""
+    import torch
+
+    from paper_2410_10503_b200 import _lib
+
+    L = _lib.load()
+    geom = m.Geometry(*g)
+    op = m.RayTransform(geom)
+    plan = op.plan().handle
+    batch, tail = 2, 1 << 16
+    need = int(L.mct_ray_workspace_bytes(plan, batch))
+    ws = torch.full((need + tail,), 0xAB, dtype=torch.uint8, device="cuda")
+    ws[:need].zero_()
+    A, B = geom.sino_shape
+    R, C = geom.image_shape
+    x = torch.randn(batch * R * C + tail // 4, device="cuda")
+    y = torch.full((batch * A * B + tail // 4,), 7.0, device="cuda")
+    img = torch.full((batch * R * C + tail // 4,), 7.0, device="cuda")
+    st = _lib.stream_handle()
+    outs = []
+    for _ in range(2):
+        _lib.check(L.mct_ray_forward(plan, _lib.ptr(x), _lib.ptr(y), batch, _lib.ptr(ws), st))
+        _lib.check(L.mct_ray_adjoint(plan, _lib.ptr(y), _lib.ptr(img), batch, _lib.ptr(ws), st))
+        outs.append((y.clone(), img.clone()))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    assert bool((ws[need:] == 0xAB).all()), "workspace tail overwritten"
+    assert bool((y[batch * A * B:] == 7.0).all()), "sinogram tail overwritten"
+    assert bool((img[batch * R * C:] == 7.0).all()), "image tail overwritten"
+    assert bool(torch.isfinite(img[:batch * R * C]).all())
