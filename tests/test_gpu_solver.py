@@ -384,3 +384,31 @@ def test_single_gate_and_uncompensated(m):
                            data)
     assert rel_l2(xn, st.x) <= ITER_TOL
     assert np.allclose(rec.objective, objs, rtol=ITER_TOL)
+
+
+@pytest.mark.parametrize("mode", ["pdhg", "spdhg"])
+def test_fused_iterations_stay_inside_workspace(m, golden_tiny, mode):
+    """K1-K4 write nothing past the engine workspace (canary tail) and give the
+    same iterate as with the engine's own workspace."""
+    import torch
+
+    from paper_2410_10503_b200.engine import Engine
+
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    cfg = tiny_config(m, G, mode, 5, epochs=4)
+    x_ref, _ = m.run(cfg, problem, diagnostics=False)
+    eng = Engine([problem.operators], [problem.data])
+    eng.set_params(cfg)
+    eng.reset()
+    if mode == "spdhg":
+        eng.set_sequences(m.draw_sequence(cfg)[None])
+    need, tail = eng.ws.numel(), 1 << 16
+    ws = torch.full((need + tail,), 0xAB, dtype=torch.uint8, device="cuda")
+    ws[:need].zero_()
+    eng.ws = ws
+    for _ in range(cfg.epochs):
+        eng.epoch(mode, problem.alpha)
+    torch.cuda.synchronize()
+    assert bool((ws[need:] == 0xAB).all()), "workspace tail overwritten"
+    assert np.array_equal(eng.x[0].double().cpu().numpy(), x_ref)
