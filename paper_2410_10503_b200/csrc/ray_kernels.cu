@@ -147,15 +147,28 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
 #define FWD_MIN_BLOCKS 12         // 12 x 4 warps resident: 40 registers for 8 loads in flight
 #endif
 
-template <int MODE>
+template <int MODE, int LPT>
 __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(FwdArgs p) {
     const int ks = p.ksplit;
     const int item = blockIdx.z / ks;
     const int part = blockIdx.z - item * ks;
-    const int a_raw = blockIdx.y * FWD_ANGLES + threadIdx.y;
+    // LPT (single-gate launches): grid (angle groups, bin tiles by distance rank, parts): every angle group's
+    // central tiles (the longest rays) are dispatched before any edge tile, so the
+    // last, partial wave holds the shortest blocks
+    // (multi-gate launches keep bins fastest: better L2 locality across gates)
+    const int btile = LPT ? [&] {
+        const int ntile = gridDim.y, c = ntile / 2, k = blockIdx.y;
+        if (k == 0) return c;
+        const int jr = k - 1, below = c, above = ntile - 1 - c;
+        const int pairs = below < above ? below : above;
+        if (jr < 2 * pairs) return (jr & 1) ? c + 1 + (jr >> 1) : c - 1 - (jr >> 1);
+        const int r = jr - 2 * pairs;
+        return below > above ? c - 1 - pairs - r : c + 1 + pairs + r;
+    }() : (int)blockIdx.x;
+    const int a_raw = (LPT ? blockIdx.x : blockIdx.y) * FWD_ANGLES + threadIdx.y;
     const bool warp_on = a_raw < p.A;        // warp-uniform; no early exit (block syncs below)
     const int a = warp_on ? a_raw : p.A - 1;
-    const int j = blockIdx.x * 32 + threadIdx.x;
+    const int j = btile * 32 + threadIdx.x;
     const bool active = warp_on && j < p.B;
     const int jj = active ? j : p.B - 1;  // idle lanes shadow the last bin (no store)
     const RayAngle ra = p.ang[a];
@@ -572,7 +585,7 @@ int choose_ksplit(int A, int B, int n) {
         int dev = 0, sms = 148, per_sm = FWD_MIN_BLOCKS;
         if (cudaGetDevice(&dev) == cudaSuccess)
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fwd_kernel<1>, 32 * FWD_ANGLES,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fwd_kernel<1, 1>, 32 * FWD_ANGLES,
                                                           0) != cudaSuccess ||
             per_sm < 1)
             per_sm = FWD_MIN_BLOCKS;
@@ -599,18 +612,32 @@ static void fwd_prefer_l1() {
 #else
     const int pct = 7;  // >= 12 blocks x 1 KB reserved of 228 KB -> the 16 KB config
 #endif
-    cudaFuncSetAttribute(fwd_kernel<0>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute(fwd_kernel<1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel<0, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel<1, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel<0, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel<1, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
 cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st) {
     fwd_prefer_l1();
-    dim3 block(32, FWD_ANGLES),
-        grid((a.B + 31) / 32, (a.A + FWD_ANGLES - 1) / FWD_ANGLES, items * a.ksplit);
+    // one single-gate item: longest-rays-first dispatch order (LPT) shrinks the
+    // last partial wave; with many items (C5 batch) the item-major order keeps
+    // better L2 locality.  Same arithmetic either way (block order only).
+    const bool lpt = a.ksplit > 1 && items == 1;
+    dim3 block(32, FWD_ANGLES);
+    const unsigned ntile = (a.B + 31) / 32, ngroup = (a.A + FWD_ANGLES - 1) / FWD_ANGLES;
+    dim3 grid(lpt ? ngroup : ntile, lpt ? ntile : ngroup, items * a.ksplit);
+    if (lpt) {
+        if (mode == 0)
+            fwd_kernel<0, 1><<<grid, block, 0, st>>>(a);
+        else
+            fwd_kernel<1, 1><<<grid, block, 0, st>>>(a);
+        return cudaGetLastError();
+    }
     if (mode == 0)
-        fwd_kernel<0><<<grid, block, 0, st>>>(a);
+        fwd_kernel<0, 0><<<grid, block, 0, st>>>(a);
     else
-        fwd_kernel<1><<<grid, block, 0, st>>>(a);
+        fwd_kernel<1, 0><<<grid, block, 0, st>>>(a);
     return cudaGetLastError();
 }
 
