@@ -557,13 +557,16 @@ __global__ void __launch_bounds__(ADJ_THREADS, ADJ_MIN_BLOCKS) adj_kernel(AdjArg
 #ifndef PACK_SMALL_ITEMS
 #define PACK_SMALL_ITEMS 1
 #endif
+#ifndef PACK16_MINB
+#define PACK16_MINB 4
+#endif
 #ifndef PACK32_MINB
 #define PACK32_MINB 6
 #endif
 cudaError_t launch_pack(const PackArgs& a, int items, cudaStream_t st) {
     if (items <= PACK_SMALL_ITEMS) {  // few gates: small tiles, one halo element per thread
         dim3 grid((a.cols + 15) / 16, (a.rows + 15) / 16, items);
-        pack_kernel<16, 320, 1><<<grid, 320, 0, st>>>(a);
+        pack_kernel<16, 320, PACK16_MINB><<<grid, 320, 0, st>>>(a);
     } else {
         dim3 grid((a.cols + 31) / 32, (a.rows + 31) / 32, items);
         pack_kernel<32, 256, PACK32_MINB><<<grid, 256, 0, st>>>(a);
