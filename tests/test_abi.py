@@ -70,3 +70,38 @@ def test_null_arguments_rejected():
         _lib.check(L.mct_reduce(None, None, 10, 1, 10, 0, None, None, None))
     with pytest.raises(ValueError):
         _lib.check(L.mct_warp_plan_create_dilatation(ctypes.byref(ctypes.c_void_p()), 4, 4, 0.0))
+
+
+def _build_c_demo(tmp_path):
+    import shutil
+    import subprocess
+
+    cc = shutil.which("cc") or shutil.which("gcc")
+    cuda = Path("/usr/local/cuda")
+    if cc is None or not (cuda / "include" / "cuda_runtime.h").exists():
+        pytest.skip("no C compiler / CUDA headers")
+    build_native()
+    root = HEADER.parent.parent
+    exe = tmp_path / "c_abi_demo"
+    cmd = [cc, "-O2", "-I", str(root / "include"), "-I", str(cuda / "include"),
+           str(root / "examples" / "c_abi_demo.c"), "-L", str(LIB_PATH.parent), "-lmctomo_b200",
+           "-L", str(cuda / "lib64"), "-lcudart", "-lm", f"-Wl,-rpath,{LIB_PATH.parent}",
+           "-o", str(exe)]
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    return exe
+
+
+def test_c_abi_demo_compiles_without_python_types(tmp_path):
+    """examples/c_abi_demo.c uses the boundary from plain C (no torch, no Python)."""
+    assert _build_c_demo(tmp_path).exists()
+
+
+@pytest.mark.gpu
+def test_c_abi_demo_runs(tmp_path):
+    import subprocess
+
+    exe = _build_c_demo(tmp_path)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "rel =" in out.stdout
