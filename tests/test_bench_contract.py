@@ -23,3 +23,34 @@ def test_reference_arm_json_line():
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0
     assert "workload" in line["config"]
+
+
+KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+        "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+        "gpu_launches", "clocks")
+
+
+def _run_bench(*args):
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], capture_output=True,
+                         text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", ["c3", "c5"])
+def test_our_arm_json_line(config):
+    line = _run_bench("--config", config, "--steps", "3", "--warmup", "3", "--no-cpu-baseline")
+    for key in KEYS:
+        assert key in line, key
+    assert line["value"] > 0 and line["unit"] == "epochs/s" and line["n_gpus"] == 1
+    r = line["roofline"]
+    assert r["bound"] == "hbm" and r["achieved"] > 0 and r["peak"] > 0
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    e = line["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert line["gpu_launches"] >= 4 * line["steps"]
+    assert "sm_mhz" in line["clocks"] and "workload" in line["config"]
