@@ -406,3 +406,18 @@ def test_no_writes_outside_buffers(m, g):
     assert bool((y[batch * A * B:] == 7.0).all()), "sinogram tail overwritten"
     assert bool((img[batch * R * C:] == 7.0).all()), "image tail overwritten"
     assert bool(torch.isfinite(img[:batch * R * C]).all())
+
+
+def test_power_method_contract_on_device(m):
+    """The reference's power-method / stacked-norm contract (test_linops.py:115-161)
+    on the device maps."""
+    assert m.power_method(m.IdentityMap((9,)), iterations=3, seed=0) == 1.0
+    op = m.DiagonalMap(np.linspace(0.1, 2.0, 11))
+    a = m.power_method(op, iterations=40, seed=5)
+    assert a == m.power_method(op, iterations=40, seed=5)
+    assert abs(a - 2.0) <= 1e-2
+    with pytest.warns(RuntimeWarning):
+        assert m.power_method(m.DiagonalMap(np.zeros(4)), iterations=10, seed=0) == 0.0
+    n = 7
+    blocks = [m.IdentityMap((5,)) for _ in range(n)]
+    assert abs(m.stacked_norm_sq(blocks, iterations=50, seed=0) - n) <= 1e-6
