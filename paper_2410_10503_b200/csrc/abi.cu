@@ -90,6 +90,10 @@ FwdArgs fwd_args(const mct_ray_plan* rp, const void* ws) {
     a.off_dy = rp->off_dy;
     a.off_part = rp->off_part;
     a.off_cnt = rp->off_cnt;
+    a.pair_block = rp->pair_block;
+    a.off_px = rp->off_px;
+    a.off_pxt = rp->off_pxt;
+    a.off_pdy = rp->off_pdy;
     a.ksplit = rp->ksplit1;
     a.wy = rp->wy;
     a.pb = rp->pb;
@@ -111,6 +115,9 @@ AdjArgs adj_args(const mct_ray_plan* rp, const void* ws) {
     a.off_dy = rp->off_dy;
     a.off_img = rp->off_img;
     a.img_slot_bytes = rp->img_slot_bytes;
+    a.pair_block = rp->pair_block;
+    a.off_pdy = rp->off_pdy;
+    a.items = 1;
     a.asplit = 1;
     return a;
 }
@@ -126,6 +133,9 @@ PackArgs pack_args(const mct_ray_plan* rp, void* ws) {
     a.item_bytes = rp->item_bytes;
     a.off_x = rp->off_x;
     a.off_xt = rp->off_xt;
+    a.pair_block = rp->pair_block;
+    a.off_px = rp->off_px;
+    a.off_pxt = rp->off_pxt;
     a.x_slice_stride = (long long)rp->rows * rp->cols;
     a.cprox = 1.0f;
     return a;
@@ -140,6 +150,7 @@ UpdArgs upd_args(const mct_ray_plan* rp, const void* ws) {
     a.item_bytes = rp->item_bytes;
     a.off_img = rp->off_img;
     a.img_slot_bytes = rp->img_slot_bytes;
+    a.pair_block = rp->pair_block;
     a.asplit = 1;
     return a;
 }
@@ -252,6 +263,16 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     off += align256((size_t)((num_angles + MCT_FWD_ANGLES - 1) / MCT_FWD_ANGLES) *
                     ((num_bins + 31) / 32) * sizeof(int));
     p->item_bytes = off;
+    // gate-pair region (interleaved float4 layouts, see mct_internal.cuh)
+    size_t poff = 0;
+    p->off_px = poff;
+    poff += align256((size_t)rows * p->wx * sizeof(float4));
+    p->off_pxt = poff;
+    poff += align256((size_t)cols * p->wxt * sizeof(float4));
+    p->off_pdy = poff;
+    poff += align256((size_t)num_angles * p->wy * sizeof(float4));
+    p->pair_bytes = poff;
+    p->pair_block = 2 * p->item_bytes + p->pair_bytes;
 
     cudaError_t e = cudaMalloc(&p->d_fwd, sizeof(RayAngle) * num_angles);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_adj, sizeof(AdjAngle) * num_angles);
@@ -279,7 +300,7 @@ int mct_ray_plan_destroy(mct_ray_plan* plan) {
 
 size_t mct_ray_workspace_bytes(const mct_ray_plan* plan, int batch) {
     if (!plan || batch < 1) return 0;
-    return plan->item_bytes * (size_t)batch;
+    return mct_ws_bytes(plan, batch);
 }
 
 int mct_ray_forward(const mct_ray_plan* rp, const float* x, float* sino, int batch, void* ws,
@@ -304,8 +325,7 @@ int mct_ray_adjoint(const mct_ray_plan* rp, const float* sino, float* img, int b
     MCT_REQUIRE(rp && sino && img && ws, "null argument");
     MCT_REQUIRE(batch >= 1, "batch must be >= 1");
     cudaStream_t st = (cudaStream_t)stream;
-    MCT_CUDA(launch_pad_sino(sino, rp->d_adj, static_cast<char*>(ws), rp->item_bytes, rp->off_dy, rp->A, rp->B,
-                             rp->wy, rp->pb, batch, st),
+    MCT_CUDA(launch_pad_sino(sino, rp, static_cast<char*>(ws), batch, st),
              "pad sinogram");
     AdjArgs aa = adj_args(rp, ws);
     aa.asplit = choose_asplit(rp, batch);
@@ -549,7 +569,7 @@ int mct_family_set_params(mct_family* fam, const double* sigmas, const double* p
 
 size_t mct_family_workspace_bytes(const mct_family* fam, int items) {
     if (!fam || items < 1) return 0;
-    return fam->ray->item_bytes * (size_t)items;
+    return mct_ws_bytes(fam->ray, items);
 }
 
 int mct_gated_forward(const mct_family* fam, int slice, int gate, const float* x, float* sino,
@@ -604,8 +624,7 @@ int mct_gated_adjoint(const mct_family* fam, int slice, int gate, const float* y
     MCT_REQUIRE(slice >= 0 && slice < fam->S && gate >= 0 && gate < fam->N, "gate out of range");
     const mct_ray_plan* rp = fam->ray;
     cudaStream_t st = (cudaStream_t)stream;
-    MCT_CUDA(launch_pad_sino(y, rp->d_adj, static_cast<char*>(ws), rp->item_bytes, rp->off_dy, rp->A, rp->B,
-                             rp->wy, rp->pb, 1, st),
+    MCT_CUDA(launch_pad_sino(y, rp, static_cast<char*>(ws), 1, st),
              "pad sinogram");
     AdjArgs aa = adj_args(rp, ws);
     aa.asplit = choose_asplit(rp, 1);

@@ -9,6 +9,16 @@
 //                        (dy[a][j], dy[a][j+1])
 // Pad regions are zero-initialised once (workspace contract) and never written,
 // so the Joseph gather loops need no bounds checks.
+//
+// Gate pairs: every launch of two or more items (PDHG: all gates; C5: a batch of
+// slices) shares one ray geometry, so K2 / K3 process items in pairs (2p, 2p+1):
+// one fixed-point walk / one set of tent weights drives both items, and one
+// 16-byte load fetches both items' pair-packed taps from a pair region in which
+// the two items' X2 / XT2 / DY2 are interleaved element by element (float4 =
+// (item 2p pair, item 2p+1 pair)).  Items are stored in pair blocks
+//   [item 2p | item 2p+1 | pair region p]   (stride pair_block)
+// so the single-item regions (single-gate SPDHG, standalone operators) and the
+// pair regions never overlap and each keeps its own zero pads.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -58,6 +68,7 @@ struct mct_ray_plan {
     RayAngle* d_fwd;
     AdjAngle* d_adj;
     size_t off_x, off_xt, off_dy, off_img, img_slot_bytes, off_part, off_cnt, item_bytes;
+    size_t off_px, off_pxt, off_pdy, pair_bytes, pair_block;  // pair region (see top)
     int ksplit1;  // K2 ray split of single-gate launches (see MCT_KSPLIT_MIN)
 };
 
@@ -81,6 +92,26 @@ struct mct_ray_plan {
 #ifndef MCT_FWD_ANGLES
 #define MCT_FWD_ANGLES 4
 #endif
+
+// Launches of >= 2 items run the gate-pair kernels (MCT_PAIRS=0 disables them).
+#ifndef MCT_PAIRS
+#define MCT_PAIRS 1
+#endif
+__host__ __device__ __forceinline__ bool mct_use_pairs(int items) { return MCT_PAIRS && items >= 2; }
+
+// Byte offset of item `item`'s region and of pair p's region in a workspace.
+__host__ __device__ __forceinline__ size_t mct_item_off(int item, size_t item_bytes,
+                                                        size_t pair_block) {
+    return (size_t)(item >> 1) * pair_block + (size_t)(item & 1) * item_bytes;
+}
+__host__ __device__ __forceinline__ size_t mct_pair_off(int pair, size_t item_bytes,
+                                                        size_t pair_block) {
+    return (size_t)pair * pair_block + 2 * item_bytes;
+}
+// Workspace bytes for launches of up to `items` items.
+inline size_t mct_ws_bytes(const mct_ray_plan* p, int items) {
+    return items <= 1 ? p->item_bytes : (size_t)((items + 1) / 2) * p->pair_block;
+}
 
 // --------------------------------------------------------------- warp plan --
 struct WarpDesc {
@@ -142,6 +173,8 @@ struct PackArgs {
     int rows, cols, wx, wxt;
     char* ws;
     size_t item_bytes, off_x, off_xt;
+    size_t pair_block, off_px, off_pxt;
+    int paired;              // write the interleaved pair region instead of the item's own
     ItemSel sel;
     int N;
     const WarpDesc* warps;   // NULL: identity; with sel.gates NULL: warps[0]
@@ -159,6 +192,8 @@ struct FwdArgs {
     double sp, jmid;
     const char* ws;
     size_t item_bytes, off_x, off_xt, off_dy, off_part, off_cnt;
+    size_t pair_block, off_px, off_pxt, off_pdy;
+    int items;               // items of the launch (pair mode: the last pair may be half)
     int ksplit;
     int wy, pb;
     ItemSel sel;
@@ -180,13 +215,15 @@ struct AdjArgs {
     double jmid;
     const char* ws;
     size_t item_bytes, off_dy, off_img, img_slot_bytes;
+    size_t pair_block, off_pdy;
+    int items;
     int asplit;
 };
 
 struct UpdArgs {
     int rows, cols;
     const char* ws;
-    size_t item_bytes, off_img, img_slot_bytes;
+    size_t item_bytes, off_img, img_slot_bytes, pair_block;
     int asplit;
     const float* img_override;  // plain D^* of a caller image (single item)
     ItemSel sel;
@@ -203,8 +240,7 @@ struct UpdArgs {
 
 // ------------------------------------------------------------- launchers --
 cudaError_t launch_pack(const PackArgs& a, int items, cudaStream_t st);
-cudaError_t launch_pad_sino(const float* sino, const AdjAngle* ang, char* ws, size_t item_bytes,
-                            size_t off_dy, int A, int B, int wy, int pb, int items,
+cudaError_t launch_pad_sino(const float* sino, const mct_ray_plan* rp, char* ws, int items,
                             cudaStream_t st);
 cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st);
 cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, cudaStream_t st);

@@ -49,9 +49,15 @@ __global__ void __launch_bounds__(THREADS, MINB) pack_kernel(PackArgs p) {
         return v;
     };
 
-    char* base = p.ws + (size_t)item * p.item_bytes;
-    float2* X = reinterpret_cast<float2*>(base + p.off_x) + MCT_PADX;
-    float2* XT = reinterpret_cast<float2*>(base + p.off_xt) + MCT_PADX;
+    // own region: element e at X[e]; pair mode: the pair region, element e of this
+    // item at X[2e + (item & 1)] (float2 halves of the interleaved float4)
+    char* base = p.paired ? p.ws + mct_pair_off(item >> 1, p.item_bytes, p.pair_block)
+                          : p.ws + mct_item_off(item, p.item_bytes, p.pair_block);
+    const int es = p.paired ? 2 : 1;
+    float2* X = reinterpret_cast<float2*>(base + (p.paired ? p.off_px : p.off_x)) + es * MCT_PADX +
+                (p.paired ? (item & 1) : 0);
+    float2* XT = reinterpret_cast<float2*>(base + (p.paired ? p.off_pxt : p.off_xt)) +
+                 es * MCT_PADX + (p.paired ? (item & 1) : 0);
 
     const int c0 = blockIdx.x * T, r0 = blockIdx.y * T;
     const int tid = threadIdx.x;
@@ -81,34 +87,40 @@ __global__ void __launch_bounds__(THREADS, MINB) pack_kernel(PackArgs p) {
         const int r = r0 + i, c = c0 + tx;
         if (r < rows && c < cols) {
             const float w = tile[i][tx];
-            X[(long long)r * p.wx + c] = make_float2(w, tile[i][tx + 1] - w);
-            if (c == 0) X[(long long)r * p.wx - 1] = make_float2(0.0f, w);
+            X[es * ((long long)r * p.wx + c)] = make_float2(w, tile[i][tx + 1] - w);
+            if (c == 0) X[es * ((long long)r * p.wx - 1)] = make_float2(0.0f, w);
         }
         // transposed: element (c, r) pairs W[r][c] with W[r+1][c]
         const int ct = c0 + i, rt = r0 + tx;
         if (rt < rows && ct < cols) {
             const float w = tile[tx][i];
-            XT[(long long)ct * p.wxt + rt] = make_float2(w, tile[tx + 1][i] - w);
-            if (rt == 0) XT[(long long)ct * p.wxt - 1] = make_float2(0.0f, w);
+            XT[es * ((long long)ct * p.wxt + rt)] = make_float2(w, tile[tx + 1][i] - w);
+            if (rt == 0) XT[es * ((long long)ct * p.wxt - 1)] = make_float2(0.0f, w);
         }
     }
 }
 
-// Copy a plain (A, B) sinogram into the pair-packed padded DY2 of each item,
-// pre-scaled by the angle's step length (A^* then only needs the tent weights).
+// Copy a plain (A, B) sinogram into the pair-packed padded DY2 of each item (or
+// the item's half of its pair region), pre-scaled by the angle's step length
+// (A^* then only needs the tent weights).
 __global__ void pad_sino_kernel(const float* __restrict__ sino, const AdjAngle* __restrict__ ang,
-                                char* ws, size_t item_bytes, size_t off_dy, int A, int B, int wy,
-                                int pb) {
+                                char* ws, size_t item_bytes, size_t pair_block, size_t off_dy,
+                                int A, int B, int wy, int pb, int paired) {
     const int item = blockIdx.z;
     const int a = blockIdx.y;
     const float step = ang[a].step;
-    float* DY = reinterpret_cast<float*>(ws + (size_t)item * item_bytes + off_dy);
+    const int G = paired ? 2 : 1;
+    float* DY = reinterpret_cast<float*>(
+                    ws + (paired ? mct_pair_off(item >> 1, item_bytes, pair_block)
+                                 : mct_item_off(item, item_bytes, pair_block)) +
+                    off_dy) +
+                (paired ? 2 * (item & 1) : 0);
     const float* s = sino + ((long long)item * A + a) * B;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x) {
-        const long long e = 2 * ((long long)a * wy + pb + j);
+        const long long e = 2 * G * ((long long)a * wy + pb + j);
         const float v = s[j] * step;
         DY[e] = v;
-        DY[e - 1] = v;
+        DY[e - 2 * G + 1] = v;
     }
 }
 
@@ -147,8 +159,10 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
 #define FWD_MIN_BLOCKS 12         // 12 x 4 warps resident: 40 registers for 8 loads in flight
 #endif
 
+// Single-item K2 (one gate per block): kept as its own kernel; the G = 1
+// instantiation of the generic kernel below schedules 20 % slower (ptxas).
 template <int MODE, int LPT>
-__global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(FwdArgs p) {
+__global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel1(FwdArgs p) {
     const int ks = p.ksplit;
     const int item = blockIdx.z / ks;
     const int part = blockIdx.z - item * ks;
@@ -172,7 +186,7 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(Fw
     const bool active = warp_on && j < p.B;
     const int jj = active ? j : p.B - 1;  // idle lanes shadow the last bin (no store)
     const RayAngle ra = p.ang[a];
-    const char* base = p.ws + (size_t)item * p.item_bytes;
+    const char* base = p.ws + mct_item_off(item, p.item_bytes, p.pair_block);
     const int cd = ra.cols_dom;
     // tap index = hi(fx) >= 0: the row pad is folded into fx so the address is one
     // unsigned 32x64 multiply-add
@@ -342,6 +356,289 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(Fw
     }
 }
 
+// Pair-packed tap vectors: G = 1 -> float2 (value, forward difference); G = 2 ->
+// float4 holding the pairs of the two items of a gate pair.
+template <int G> struct TapVec;
+template <> struct TapVec<1> { using T = float2; };
+template <> struct TapVec<2> { using T = float4; };
+__device__ __forceinline__ float tv(const float2& v, int) { return v.x; }
+__device__ __forceinline__ float td(const float2& v, int) { return v.y; }
+__device__ __forceinline__ float tv(const float4& v, int h) { return h ? v.z : v.x; }
+__device__ __forceinline__ float td(const float4& v, int h) { return h ? v.w : v.y; }
+
+#ifndef FWD_MIN_BLOCKS2
+#define FWD_MIN_BLOCKS2 8
+#endif
+#ifndef FWD_PAIR_ORDER
+#define FWD_PAIR_ORDER 1  // 1: gate-pair K2 consumes sample by sample (see the core loop)
+#endif
+
+// G = 2: one warp walks the rays of two items (a gate pair) at once; every
+// per-item sum is accumulated exactly as with G = 1 (bitwise equal results).
+template <int MODE, int LPT, int G>
+__global__ void __launch_bounds__(32 * FWD_ANGLES, G == 1 ? FWD_MIN_BLOCKS : FWD_MIN_BLOCKS2)
+    fwd_kernel(FwdArgs p) {
+    using V = typename TapVec<G>::T;
+    const int ks = p.ksplit;
+    const int group = blockIdx.z / ks;  // item (G = 1) or gate pair (G = 2)
+    const int part = blockIdx.z - group * ks;
+    // LPT (single-gate launches): grid (angle groups, bin tiles by distance rank, parts): every angle group's
+    // central tiles (the longest rays) are dispatched before any edge tile, so the
+    // last, partial wave holds the shortest blocks
+    // (multi-gate launches keep bins fastest: better L2 locality across gates)
+    const int btile = LPT ? [&] {
+        const int ntile = gridDim.y, c = ntile / 2, k = blockIdx.y;
+        if (k == 0) return c;
+        const int jr = k - 1, below = c, above = ntile - 1 - c;
+        const int pairs = below < above ? below : above;
+        if (jr < 2 * pairs) return (jr & 1) ? c + 1 + (jr >> 1) : c - 1 - (jr >> 1);
+        const int r = jr - 2 * pairs;
+        return below > above ? c - 1 - pairs - r : c + 1 + pairs + r;
+    }() : (int)blockIdx.x;
+    const int a_raw = (LPT ? blockIdx.x : blockIdx.y) * FWD_ANGLES + threadIdx.y;
+    const bool warp_on = a_raw < p.A;        // warp-uniform; no early exit (block syncs below)
+    const int a = warp_on ? a_raw : p.A - 1;
+    const int j = btile * 32 + threadIdx.x;
+    const bool active = warp_on && j < p.B;
+    const int jj = active ? j : p.B - 1;  // idle lanes shadow the last bin (no store)
+    const RayAngle ra = p.ang[a];
+    const int item0 = G * group;
+    const char* base0 = p.ws + mct_item_off(item0, p.item_bytes, p.pair_block);  // counters
+    const char* tb = G == 1 ? base0 : p.ws + mct_pair_off(group, p.item_bytes, p.pair_block);
+    const int cd = ra.cols_dom;
+    // tap index = hi(fx) >= 0: the row pad is folded into fx so the address is one
+    // unsigned 32x64 multiply-add
+    const V* __restrict__ X2 = reinterpret_cast<const V*>(
+        tb + (G == 1 ? (cd ? p.off_xt : p.off_x) : (cd ? p.off_pxt : p.off_px)));
+    const int stride = cd ? p.wxt : p.wx;
+    const int nmaj = cd ? p.cols : p.rows;
+    const int lim = cd ? p.rows : p.cols;
+
+    // per-ray range of dominant-axis samples that can have a tap inside the grid
+    const double sj = ((double)jj - p.jmid) * p.sp;
+    const double c0 = ra.P * sj + ra.Q;
+    int lo = nmaj, hi = -1;
+    if (ra.slope == 0.0) {
+        if (c0 > -1.0 && c0 < (double)lim) { lo = 0; hi = nmaj - 1; }
+    } else {
+        const double ka = (-1.0 - c0) / ra.slope, kb = ((double)lim - c0) / ra.slope;
+        const double top = (double)nmaj + 2.0;
+        const double kmin = fmin(fmax(fmin(ka, kb), -2.0), top);
+        const double kmax = fmin(fmax(fmax(ka, kb), -2.0), top);
+        lo = max(0, (int)floor(kmin));
+        hi = min(nmaj - 1, (int)ceil(kmax));
+    }
+    int wlo = __reduce_min_sync(0xffffffffu, lo);  // union of the warp's ranges
+    int whi = __reduce_max_sync(0xffffffffu, hi);
+    int clo = __reduce_max_sync(0xffffffffu, lo);        // common core
+    int chi = __reduce_min_sync(0xffffffffu, hi);
+    // this block's share of the walk: part `part` of ks equal pieces
+    const int wlen = whi - wlo + 1;
+    const int k_lo = wlo + (int)((long long)wlen * part / ks);
+    const int k_hi = wlo + (int)((long long)wlen * (part + 1) / ks) - 1;
+    wlo = k_lo;
+    whi = k_hi;
+    clo = max(clo, k_lo);
+    chi = min(chi, k_hi);
+    double tot[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) tot[h] = 0.0;
+    if (warp_on && wlo <= whi) {
+        if (clo > chi) { clo = whi + 1; chi = whi; }     // no common core: all edge
+        const long long inc64 = ra.slope_fx + ((long long)stride << 32);
+        const unsigned ilo = (unsigned)inc64, ihi = (unsigned)(inc64 >> 32);
+        const long long fx0 = __double2ll_rn((c0 + (double)wlo * ra.slope) * FX_ONE) +
+                              ((long long)(wlo * stride + MCT_PADX) << 32);
+        unsigned flo = (unsigned)fx0, fhi = (unsigned)(fx0 >> 32);
+        int rowoff = wlo * stride + MCT_PADX;
+        const unsigned lim1 = (unsigned)(lim + 1);
+        double dacc[G];
+        float ea[G];  // ragged-edge samples (predicated on the tap range)
+#pragma unroll
+        for (int h = 0; h < G; ++h) { dacc[h] = 0.0; ea[h] = 0.0f; }
+        int k = wlo;
+        for (; k < clo; ++k) {
+            const int i0 = (int)fhi - rowoff;
+            if ((unsigned)(i0 + 1) < lim1) {
+                const V v = __ldg(X2 + fhi);
+                const float f = (float)(flo >> 8) * INV_2_24;
+#pragma unroll
+                for (int h = 0; h < G; ++h) ea[h] += fmaf(f, td(v, h), tv(v, h));
+            }
+            fx_add(flo, fhi, ilo, ihi);
+            rowoff += stride;
+        }
+        // core: every lane's taps are inside the padded row (pads read zero)
+        for (int kc = k; kc <= chi; kc += 64) {
+            const int kend = min(chi, kc + 63);
+            float s[G][4], t[G][4];  // sums of v0 and of frac*2^24*(x[i+1] - x[i])
+#pragma unroll
+            for (int h = 0; h < G; ++h)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) s[h][q] = t[h][q] = 0.0f;
+            int kk = kc;
+            // 8 samples per trip: all 8 loads are issued before the first use
+            for (; kk + 7 <= kend; kk += 8) {
+                unsigned lo8[8], hi8[8];
+                lo8[0] = flo;
+                hi8[0] = fhi;
+#pragma unroll
+                for (int u = 1; u < 8; ++u) {
+                    lo8[u] = lo8[u - 1];
+                    hi8[u] = hi8[u - 1];
+                    fx_add(lo8[u], hi8[u], ilo, ihi);
+                }
+                V v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldg(X2 + hi8[u]);
+                flo = lo8[7];
+                fhi = hi8[7];
+                fx_add(flo, fhi, ilo, ihi);
+                // consumption order steers ptxas' schedule under the register cap:
+                // values of a half-trip first, then its differences (G = 1: 20 %
+                // faster single-gate K2 than sample-by-sample consumption)
+                if (G == 1 || FWD_PAIR_ORDER == 0) {
+#pragma unroll
+                    for (int hb = 0; hb < 2; ++hb) {
+#pragma unroll
+                        for (int h = 0; h < G; ++h)
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) s[h][q] += tv(v[4 * hb + q], h);
+#pragma unroll
+                        for (int h = 0; h < G; ++h)
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                t[h][q] = fmaf((float)(lo8[4 * hb + q] >> 8), td(v[4 * hb + q], h),
+                                               t[h][q]);
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const float f = (float)(lo8[u] >> 8);
+#pragma unroll
+                        for (int h = 0; h < G; ++h) {
+                            s[h][u & 3] += tv(v[u], h);
+                            t[h][u & 3] = fmaf(f, td(v[u], h), t[h][u & 3]);
+                        }
+                    }
+                }
+            }
+            for (; kk <= kend; ++kk) {
+                const V v0 = __ldg(X2 + fhi);
+                const float f = (float)(flo >> 8);
+#pragma unroll
+                for (int h = 0; h < G; ++h) {
+                    s[h][0] += tv(v0, h);
+                    t[h][0] = fmaf(f, td(v0, h), t[h][0]);
+                }
+                fx_add(flo, fhi, ilo, ihi);
+            }
+#pragma unroll
+            for (int h = 0; h < G; ++h)
+                dacc[h] += (double)((s[h][0] + s[h][1]) + (s[h][2] + s[h][3])) +
+                           (double)((t[h][0] + t[h][1]) + (t[h][2] + t[h][3])) * (double)INV_2_24;
+            k = kend + 1;
+        }
+        rowoff = k * stride + MCT_PADX;
+        for (; k <= whi; ++k) {
+            const int i0 = (int)fhi - rowoff;
+            if ((unsigned)(i0 + 1) < lim1) {
+                const V v = __ldg(X2 + fhi);
+                const float f = (float)(flo >> 8) * INV_2_24;
+#pragma unroll
+                for (int h = 0; h < G; ++h) ea[h] += fmaf(f, td(v, h), tv(v, h));
+            }
+            fx_add(flo, fhi, ilo, ihi);
+            rowoff += stride;
+        }
+#pragma unroll
+        for (int h = 0; h < G; ++h) tot[h] = dacc[h] + (double)ea[h];
+    }
+    // items of this block (the second half of a last, odd pair is a dummy)
+    const int nval = G == 1 ? 1 : min(G, p.items - item0);
+    double sum[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) sum[h] = tot[h];
+    if (ks > 1) {
+        // combine the parts: the last block of this tile to arrive sums them in order
+        if (active) {
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+                if (h < nval) {
+                    double* PART = reinterpret_cast<double*>(
+                        const_cast<char*>(p.ws) + mct_item_off(item0 + h, p.item_bytes, p.pair_block) +
+                        p.off_part);
+                    PART[((long long)part * p.A + a) * p.B + j] = tot[h];
+                }
+            }
+        }
+        __shared__ int s_last;
+        __syncthreads();
+        if (threadIdx.x == 0 && threadIdx.y == 0) {
+            int* cnt = reinterpret_cast<int*>(const_cast<char*>(base0) + p.off_cnt) +
+                       blockIdx.y * gridDim.x + blockIdx.x;
+#if FWD_ACQREL
+            // release: the block's PART stores (ordered before by the barrier);
+            // acquire: the other parts' stores, for the last block to arrive
+            int prev;
+            asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                         : "=r"(prev) : "l"(cnt) : "memory");
+#else
+            __threadfence();
+            const int prev = atomicAdd(cnt, 1);
+#endif
+            s_last = (prev == ks - 1);
+            if (s_last) *cnt = 0;  // every part has arrived: re-arm for the next launch
+        }
+        __syncthreads();
+        if (!s_last || !active) return;
+#if !FWD_ACQREL
+        __threadfence();
+#endif
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            if (h < nval) {
+                const double* PART = reinterpret_cast<const double*>(
+                    p.ws + mct_item_off(item0 + h, p.item_bytes, p.pair_block) + p.off_part);
+                double acc = 0.0;
+                for (int q = 0; q < ks; ++q) acc += __ldcg(PART + ((long long)q * p.A + a) * p.B + j);
+                sum[h] = acc;
+            }
+        }
+    } else if (!active) {
+        return;
+    }
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+        if (h >= nval) break;
+        const int item = item0 + h;
+        const float proj = (float)sum[h] * ra.step;
+        if (MODE == 0) {
+            p.out[(long long)item * p.out_item_stride + (long long)a * p.B + j] = proj;
+        } else {
+            int slice, gate, iter;
+            resolve_item(p.sel, item, slice, gate, iter);
+            const long long off = (((long long)slice * p.N + gate) * p.A + a) * p.B + j;
+            const GateParam gp = p.gp[gate];
+            const float yv = p.y[off];
+            const float dv = __ldg(p.d + off);
+            const float yn = (fmaf(gp.sigma, proj, yv) - gp.sigma * dv) * gp.dual_inv;
+            p.y[off] = yn;
+            // DY2 element j (pair of item `item`): own region (G = 1) or the item's
+            // half of the pair region's float4 element (G = 2)
+            float* DY = reinterpret_cast<float*>(const_cast<char*>(tb) +
+                                                 (G == 1 ? p.off_dy : p.off_pdy)) + 2 * h;
+            const long long e = 2 * G * ((long long)a * p.wy + p.pb + j);
+            const float dlt = (yn - yv) * ra.step;  // pre-scaled for A^* (see K3)
+            DY[e] = dlt;
+            DY[e - 2 * G + 1] = dlt;
+            if (p.proj) p.proj[off] = proj;
+            if (!isfinite(yn) && p.status)
+                atomicMin(p.status + 1, ((unsigned long long)iter << 20) | (unsigned long long)gate);
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K3: A^* as a deterministic transpose-gather (no atomics).  Pixel (r, c) at
 // angle a receives  step * max(0, 1 - |j - jc|*g) * dy[a, j]  from the bins j
@@ -370,7 +667,6 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(Fw
 #ifndef ADJ_WARPS
 #define ADJ_WARPS 4
 #endif
-#define ADJ_TH (ADJ_PPT * ADJ_WARPS)
 #define ADJ_THREADS (ADJ_TW * ADJ_WARPS)
 #ifndef ADJ_CH
 #define ADJ_CH ADJ_THREADS
@@ -383,88 +679,118 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel(Fw
 #endif
 #define INV_2_32 2.3283064365386963e-10f
 
-// Tent weights of bins floor(jc) .. for a pixel whose jc has fraction tlo/2^32,
-// applied to two sinogram rows (pixel and mirror pixel).
 // One tent (bin index thi, fraction tlo/2^32) applied to two sinogram rows: row
-// thi's (pixel p at angle a) and row thi + delta's (the mirror of p at A-a).
-template <int K>
-__device__ __forceinline__ void adj_tap2(const float2* __restrict__ DY2, unsigned tlo, int thi,
-                                         int delta, float g32, float omg, float& acc_a,
-                                         float& acc_b) {
+// thi's (pixel p at angle a) and row thi + delta's (the mirror of p at A-a), for
+// the G items whose pair-packed rows share the float2 / float4 elements.
+template <int K, int G>
+__device__ __forceinline__ void adj_tap2(const typename TapVec<G>::T* __restrict__ DY2, unsigned tlo,
+                                         int thi, int delta, float g32, float omg, float* acc_a,
+                                         float* acc_b) {
+    using V = typename TapVec<G>::T;
     const float F = (float)tlo;
     if (K == 0) {
-        const float2 v = __ldg(DY2 + (unsigned)thi);
-        const float2 vm = __ldg(DY2 + (unsigned)(thi + delta));
+        const V v = __ldg(DY2 + (unsigned)thi);
+        const V vm = __ldg(DY2 + (unsigned)(thi + delta));
         const float w0 = __saturatef(fmaf(-F, g32, 1.0f));  // bin floor(jc)
         const float w1 = __saturatef(fmaf(F, g32, omg));    // bin floor(jc) + 1
-        acc_a = fmaf(w0, v.x, fmaf(w1, v.y, acc_a));
-        acc_b = fmaf(w0, vm.x, fmaf(w1, vm.y, acc_b));
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            acc_a[h] = fmaf(w0, tv(v, h), fmaf(w1, td(v, h), acc_a[h]));
+            acc_b[h] = fmaf(w0, tv(vm, h), fmaf(w1, td(vm, h), acc_b[h]));
+        }
     } else {
         const float d = F * INV_2_32;
         const float g = g32 * 4294967296.0f;
 #pragma unroll
         for (int mm = -K; mm <= K; mm += 2) {
-            const float2 v = __ldg(DY2 + (thi + mm));
-            const float2 vm = __ldg(DY2 + (thi + delta + mm));
+            const V v = __ldg(DY2 + (thi + mm));
+            const V vm = __ldg(DY2 + (thi + delta + mm));
             const float wa = __saturatef(fmaf(-fabsf((float)mm - d), g, 1.0f));
             const float wb = __saturatef(fmaf(-fabsf((float)(mm + 1) - d), g, 1.0f));
-            acc_a = fmaf(wa, v.x, fmaf(wb, v.y, acc_a));
-            acc_b = fmaf(wa, vm.x, fmaf(wb, vm.y, acc_b));
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+                acc_a[h] = fmaf(wa, tv(v, h), fmaf(wb, td(v, h), acc_a[h]));
+                acc_b[h] = fmaf(wa, tv(vm, h), fmaf(wb, td(vm, h), acc_b[h]));
+            }
         }
     }
 }
 
-template <int K>
-__device__ __forceinline__ void adj_tap1(const float2* __restrict__ DY2, unsigned tlo, int thi,
-                                         float g32, float omg, float& acc) {
+template <int K, int G>
+__device__ __forceinline__ void adj_tap1(const typename TapVec<G>::T* __restrict__ DY2, unsigned tlo,
+                                         int thi, float g32, float omg, float* acc) {
+    using V = typename TapVec<G>::T;
     const float F = (float)tlo;
     if (K == 0) {
-        const float2 v = __ldg(DY2 + (unsigned)thi);
+        const V v = __ldg(DY2 + (unsigned)thi);
         const float w0 = __saturatef(fmaf(-F, g32, 1.0f));
         const float w1 = __saturatef(fmaf(F, g32, omg));
-        acc = fmaf(w0, v.x, fmaf(w1, v.y, acc));
+#pragma unroll
+        for (int h = 0; h < G; ++h) acc[h] = fmaf(w0, tv(v, h), fmaf(w1, td(v, h), acc[h]));
     } else {
         const float d = F * INV_2_32;
         const float g = g32 * 4294967296.0f;
 #pragma unroll
         for (int mm = -K; mm <= K; mm += 2) {
-            const float2 v = __ldg(DY2 + (thi + mm));
+            const V v = __ldg(DY2 + (thi + mm));
             const float wa = __saturatef(fmaf(-fabsf((float)mm - d), g, 1.0f));
             const float wb = __saturatef(fmaf(-fabsf((float)(mm + 1) - d), g, 1.0f));
-            acc = fmaf(wa, v.x, fmaf(wb, v.y, acc));
+#pragma unroll
+            for (int h = 0; h < G; ++h) acc[h] = fmaf(wa, tv(v, h), fmaf(wb, td(v, h), acc[h]));
         }
     }
 }
 
-template <int K>
-__global__ void __launch_bounds__(ADJ_THREADS, ADJ_MIN_BLOCKS) adj_kernel(AdjArgs p) {
+#ifndef ADJ_PPT2
+#define ADJ_PPT2 4     // rows per thread of the gate-pair kernel (= ADJ_PPT: same tiles, so a
+                       // batch and a single item agree bitwise)
+#endif
+#ifndef ADJ_MIN_BLOCKS2
+#define ADJ_MIN_BLOCKS2 6
+#endif
+template <int G> struct AdjShape;
+template <> struct AdjShape<1> { static constexpr int PPT = ADJ_PPT, MINB = ADJ_MIN_BLOCKS; };
+template <> struct AdjShape<2> { static constexpr int PPT = ADJ_PPT2, MINB = ADJ_MIN_BLOCKS2; };
+
+// G = 2: a thread owns its pixels in the two items of a gate pair; the bins and
+// tent weights are computed once and applied to both items' rows (one 16-byte
+// load per pixel-angle).  Per-item arithmetic identical to G = 1.
+template <int K, int G>
+__global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(AdjArgs p) {
+    using V = typename TapVec<G>::T;
+    constexpr int PPT = AdjShape<G>::PPT;
+    constexpr int TH = PPT * ADJ_WARPS;
     __shared__ longlong2 s_t[ADJ_CH];  // anchor (with sinogram row base of a), cos/sp
     __shared__ int4 s_u[ADJ_CH];       // sin/sp (lo, hi), g*2^-32, 1 - g
     __shared__ int s_d[ADJ_CH];        // sinogram offset of row A-a relative to row a
-    __shared__ double s_tot[2 * ADJ_PPT][ADJ_THREADS];
-    const int item = blockIdx.z / p.asplit;
-    const int split = blockIdx.z - item * p.asplit;
+    __shared__ double s_tot[G][2 * PPT][ADJ_THREADS];
+    const int group = blockIdx.z / p.asplit;
+    const int split = blockIdx.z - group * p.asplit;
     const int A = p.A;
     const int npairs = (A - 1) / 2;  // pairs (a, A-a), a = 1 .. npairs
     const int q_beg = 1 + (int)((long long)npairs * split / p.asplit);
     const int q_end = 1 + (int)((long long)npairs * (split + 1) / p.asplit);
     const int tid = threadIdx.y * ADJ_TW + threadIdx.x;
     const int ncl = (p.cols + 1) >> 1;                      // left-half columns (incl. centre)
-    const int r0 = blockIdx.y * ADJ_TH, c0 = blockIdx.x * ADJ_TW;
+    const int r0 = blockIdx.y * TH, c0 = blockIdx.x * ADJ_TW;
     const int c = c0 + threadIdx.x;                          // primary column
     const int cm = p.cols - 1 - c;                           // mirror column
-    const int rt = r0 + threadIdx.y * ADJ_PPT;
-    const int nrows = min(ADJ_PPT, p.rows - rt);             // warp-uniform
+    const int rt = r0 + threadIdx.y * PPT;
+    const int nrows = min(PPT, p.rows - rt);                 // warp-uniform
     const int txc = min((int)threadIdx.x, ncl - 1 - c0);     // clamp lanes past the half
     const int cmc = p.cols - 1 - (c0 + txc);                 // (clamped) mirror column
     const double u0 = (double)r0 - 0.5 * (double)(p.rows - 1);
     const double v0 = (double)c0 - 0.5 * (double)(p.cols - 1);
-    const char* base = p.ws + (size_t)item * p.item_bytes;
-    const float2* __restrict__ DY2 = reinterpret_cast<const float2*>(base + p.off_dy);
-    const long long row_off = (long long)(threadIdx.y * ADJ_PPT);
+    const int item0 = G * group;
+    const char* tb = G == 1 ? p.ws + mct_item_off(item0, p.item_bytes, p.pair_block)
+                            : p.ws + mct_pair_off(group, p.item_bytes, p.pair_block);
+    const V* __restrict__ DY2 = reinterpret_cast<const V*>(tb + (G == 1 ? p.off_dy : p.off_pdy));
+    const long long row_off = (long long)(threadIdx.y * PPT);
 
 #pragma unroll
-    for (int m = 0; m < 2 * ADJ_PPT; ++m) s_tot[m][tid] = 0.0;
+    for (int h = 0; h < G; ++h)
+#pragma unroll
+        for (int m = 0; m < 2 * PPT; ++m) s_tot[h][m][tid] = 0.0;
 
     // ---- self-paired angles 0 and A/2 (split 0 only), pixel by pixel
     if (split == 0) {
@@ -479,11 +805,16 @@ __global__ void __launch_bounds__(ADJ_THREADS, ADJ_MIN_BLOCKS) adj_kernel(AdjArg
             long long T = TA + (long long)txc * aa.csx - row_off * aa.snx;
             long long Tm = TA + (long long)(cmc - c0) * aa.csx - row_off * aa.snx;
             for (int m = 0; m < nrows; ++m) {
-                float acc = 0.0f, accm = 0.0f;
-                adj_tap1<K>(DY2, (unsigned)T, (int)(T >> 32), g32, omg, acc);
-                adj_tap1<K>(DY2, (unsigned)Tm, (int)(Tm >> 32), g32, omg, accm);
-                s_tot[m][tid] += (double)acc;
-                s_tot[ADJ_PPT + m][tid] += (double)accm;
+                float acc[G], accm[G];
+#pragma unroll
+                for (int h = 0; h < G; ++h) acc[h] = accm[h] = 0.0f;
+                adj_tap1<K, G>(DY2, (unsigned)T, (int)(T >> 32), g32, omg, acc);
+                adj_tap1<K, G>(DY2, (unsigned)Tm, (int)(Tm >> 32), g32, omg, accm);
+#pragma unroll
+                for (int h = 0; h < G; ++h) {
+                    s_tot[h][m][tid] += (double)acc[h];
+                    s_tot[h][PPT + m][tid] += (double)accm[h];
+                }
                 T -= aa.snx;
                 Tm -= aa.snx;
             }
@@ -507,9 +838,11 @@ __global__ void __launch_bounds__(ADJ_THREADS, ADJ_MIN_BLOCKS) adj_kernel(AdjArg
         }
         __syncthreads();
         if (nrows <= 0) continue;
-        float acc[ADJ_PPT], accm[ADJ_PPT];
+        float acc[PPT][G], accm[PPT][G];
 #pragma unroll
-        for (int m = 0; m < ADJ_PPT; ++m) acc[m] = accm[m] = 0.0f;
+        for (int m = 0; m < PPT; ++m)
+#pragma unroll
+            for (int h = 0; h < G; ++h) acc[m][h] = accm[m][h] = 0.0f;
 #pragma unroll 2
         for (int t = 0; t < cnt; ++t) {
             const longlong2 T2 = s_t[t];
@@ -523,31 +856,38 @@ __global__ void __launch_bounds__(ADJ_THREADS, ADJ_MIN_BLOCKS) adj_kernel(AdjArg
             unsigned tlo = (unsigned)T, thi = (unsigned)(T >> 32);
             unsigned mlo = (unsigned)Tm, mhi = (unsigned)(Tm >> 32);
 #pragma unroll
-            for (int m = 0; m < ADJ_PPT; ++m) {
+            for (int m = 0; m < PPT; ++m) {
                 if (m < nrows) {
-                    adj_tap2<K>(DY2, tlo, (int)thi, delta, g32, omg, acc[m], accm[m]);
-                    adj_tap2<K>(DY2, mlo, (int)mhi, delta, g32, omg, accm[m], acc[m]);
+                    adj_tap2<K, G>(DY2, tlo, (int)thi, delta, g32, omg, acc[m], accm[m]);
+                    adj_tap2<K, G>(DY2, mlo, (int)mhi, delta, g32, omg, accm[m], acc[m]);
                 }
                 fx_sub(tlo, thi, (unsigned)U.x, (unsigned)U.y);
                 fx_sub(mlo, mhi, (unsigned)U.x, (unsigned)U.y);
             }
         }
 #pragma unroll
-        for (int m = 0; m < ADJ_PPT; ++m) {
-            s_tot[m][tid] += (double)acc[m];
-            s_tot[ADJ_PPT + m][tid] += (double)accm[m];
-        }
+        for (int m = 0; m < PPT; ++m)
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+                s_tot[h][m][tid] += (double)acc[m][h];
+                s_tot[h][PPT + m][tid] += (double)accm[m][h];
+            }
     }
     if (c >= ncl) return;
-    float* IMG = reinterpret_cast<float*>(const_cast<char*>(base) + p.off_img +
-                                          (size_t)split * p.img_slot_bytes);
-    for (int m = 0; m < nrows; ++m) {
-        const long long row = (long long)(rt + m) * p.cols;
-        if (cm == c) {  // centre column of an odd width: the primary role already
-            IMG[row + c] = (float)s_tot[m][tid];  // holds every angle (mirror = duplicate)
-        } else {
-            IMG[row + c] = (float)s_tot[m][tid];
-            IMG[row + cm] = (float)s_tot[ADJ_PPT + m][tid];
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+        if (G > 1 && item0 + h >= p.items) break;  // dummy half of a last, odd pair
+        float* IMG = reinterpret_cast<float*>(
+            const_cast<char*>(p.ws) + mct_item_off(item0 + h, p.item_bytes, p.pair_block) +
+            p.off_img + (size_t)split * p.img_slot_bytes);
+        for (int m = 0; m < nrows; ++m) {
+            const long long row = (long long)(rt + m) * p.cols;
+            if (cm == c) {  // centre column of an odd width: the primary role already
+                IMG[row + c] = (float)s_tot[h][m][tid];  // holds every angle (mirror = duplicate)
+            } else {
+                IMG[row + c] = (float)s_tot[h][m][tid];
+                IMG[row + cm] = (float)s_tot[h][PPT + m][tid];
+            }
         }
     }
 }
@@ -563,7 +903,9 @@ __global__ void __launch_bounds__(ADJ_THREADS, ADJ_MIN_BLOCKS) adj_kernel(AdjArg
 #ifndef PACK32_MINB
 #define PACK32_MINB 6
 #endif
-cudaError_t launch_pack(const PackArgs& a, int items, cudaStream_t st) {
+cudaError_t launch_pack(const PackArgs& a_in, int items, cudaStream_t st) {
+    PackArgs a = a_in;
+    a.paired = mct_use_pairs(items) ? 1 : 0;
     if (items <= PACK_SMALL_ITEMS) {  // few gates: small tiles, one halo element per thread
         dim3 grid((a.cols + 15) / 16, (a.rows + 15) / 16, items);
         pack_kernel<16, 320, PACK16_MINB><<<grid, 320, 0, st>>>(a);
@@ -574,11 +916,13 @@ cudaError_t launch_pack(const PackArgs& a, int items, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_pad_sino(const float* sino, const AdjAngle* ang, char* ws, size_t item_bytes,
-                            size_t off_dy, int A, int B, int wy, int pb, int items,
+cudaError_t launch_pad_sino(const float* sino, const mct_ray_plan* rp, char* ws, int items,
                             cudaStream_t st) {
-    dim3 block(256), grid((B + 255) / 256, A, items);
-    pad_sino_kernel<<<grid, block, 0, st>>>(sino, ang, ws, item_bytes, off_dy, A, B, wy, pb);
+    dim3 block(256), grid((rp->B + 255) / 256, rp->A, items);
+    const bool paired = mct_use_pairs(items);
+    pad_sino_kernel<<<grid, block, 0, st>>>(sino, rp->d_adj, ws, rp->item_bytes, rp->pair_block,
+                                            paired ? rp->off_pdy : rp->off_dy, rp->A, rp->B,
+                                            rp->wy, rp->pb, paired ? 1 : 0);
     return cudaGetLastError();
 }
 
@@ -588,7 +932,7 @@ int choose_ksplit(int A, int B, int n) {
         int dev = 0, sms = 148, per_sm = FWD_MIN_BLOCKS;
         if (cudaGetDevice(&dev) == cudaSuccess)
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fwd_kernel<1, 1>, 32 * FWD_ANGLES,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fwd_kernel1<1, 1>, 32 * FWD_ANGLES,
                                                           0) != cudaSuccess ||
             per_sm < 1)
             per_sm = FWD_MIN_BLOCKS;
@@ -615,32 +959,44 @@ static void fwd_prefer_l1() {
 #else
     const int pct = 7;  // >= 12 blocks x 1 KB reserved of 228 KB -> the 16 KB config
 #endif
-    cudaFuncSetAttribute(fwd_kernel<0, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute(fwd_kernel<1, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute(fwd_kernel<0, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute(fwd_kernel<1, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel1<0, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel1<1, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel1<0, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel1<1, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel<0, 0, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel<1, 0, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
-cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st) {
+cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st) {
     fwd_prefer_l1();
+    FwdArgs a = a_in;
+    a.items = items;
+    dim3 block(32, FWD_ANGLES);
+    const unsigned ntile = (a.B + 31) / 32, ngroup = (a.A + FWD_ANGLES - 1) / FWD_ANGLES;
+    if (mct_use_pairs(items)) {  // gate pairs (bins fastest: L2 locality across pairs)
+        dim3 grid(ntile, ngroup, ((items + 1) / 2) * a.ksplit);
+        if (mode == 0)
+            fwd_kernel<0, 0, 2><<<grid, block, 0, st>>>(a);
+        else
+            fwd_kernel<1, 0, 2><<<grid, block, 0, st>>>(a);
+        return cudaGetLastError();
+    }
     // one single-gate item: longest-rays-first dispatch order (LPT) shrinks the
     // last partial wave; with many items (C5 batch) the item-major order keeps
     // better L2 locality.  Same arithmetic either way (block order only).
     const bool lpt = a.ksplit > 1 && items == 1;
-    dim3 block(32, FWD_ANGLES);
-    const unsigned ntile = (a.B + 31) / 32, ngroup = (a.A + FWD_ANGLES - 1) / FWD_ANGLES;
     dim3 grid(lpt ? ngroup : ntile, lpt ? ntile : ngroup, items * a.ksplit);
     if (lpt) {
         if (mode == 0)
-            fwd_kernel<0, 1><<<grid, block, 0, st>>>(a);
+            fwd_kernel1<0, 1><<<grid, block, 0, st>>>(a);
         else
-            fwd_kernel<1, 1><<<grid, block, 0, st>>>(a);
+            fwd_kernel1<1, 1><<<grid, block, 0, st>>>(a);
         return cudaGetLastError();
     }
     if (mode == 0)
-        fwd_kernel<0, 0><<<grid, block, 0, st>>>(a);
+        fwd_kernel1<0, 0><<<grid, block, 0, st>>>(a);
     else
-        fwd_kernel<1, 0><<<grid, block, 0, st>>>(a);
+        fwd_kernel1<1, 0><<<grid, block, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -649,19 +1005,7 @@ cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st) {
 // split keeps >= MCT_ASPLIT_MIN_PAIRS angle pairs.
 static inline int adj_tiles_x(int cols) { return ((cols + 1) / 2 + ADJ_TW - 1) / ADJ_TW; }
 
-int choose_asplit(const mct_ray_plan* rp, int items) {
-    static int slots = 0;  // resident adj blocks per GPU (queried once)
-    if (slots == 0) {
-        int dev = 0, sms = 148, per_sm = 8;
-        if (cudaGetDevice(&dev) == cudaSuccess)
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_kernel<0>, ADJ_THREADS, 0) !=
-                cudaSuccess || per_sm < 1)
-            per_sm = 8;
-        slots = sms * per_sm;
-    }
-    const long long tiles = (long long)adj_tiles_x(rp->cols) * ((rp->rows + ADJ_TH - 1) / ADJ_TH) *
-                            (items > 0 ? items : 1);
+static int adj_split_for(long long tiles, long long slots, const mct_ray_plan* rp) {
     // >= MCT_ASPLIT_MIN_PAIRS angle pairs per split
     const long long by_angles =
         rp->A / (2 * MCT_ASPLIT_MIN_PAIRS) > 0 ? rp->A / (2 * MCT_ASPLIT_MIN_PAIRS) : 1;
@@ -691,15 +1035,60 @@ int choose_asplit(const mct_ray_plan* rp, int items) {
 #endif
 }
 
-cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, cudaStream_t st) {
-    dim3 block(ADJ_TW, ADJ_WARPS),
-        grid(adj_tiles_x(a.cols), (a.rows + ADJ_TH - 1) / ADJ_TH, items * a.asplit);
-    switch (kfoot) {
-        case 0: adj_kernel<0><<<grid, block, 0, st>>>(a); break;
-        case 1: adj_kernel<1><<<grid, block, 0, st>>>(a); break;
-        case 2: adj_kernel<2><<<grid, block, 0, st>>>(a); break;
-        case 3: adj_kernel<3><<<grid, block, 0, st>>>(a); break;
-        default: return cudaErrorInvalidValue;
+static long long adj_slots(int G) {
+    static long long slots[3] = {0, 0, 0};  // resident adj blocks per GPU (queried once)
+    if (slots[G] == 0) {
+        int dev = 0, sms = 148, per_sm = 8;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const cudaError_t e =
+            G == 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_kernel<0, 1>, ADJ_THREADS, 0)
+                   : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_kernel<0, 2>, ADJ_THREADS, 0);
+        if (e != cudaSuccess || per_sm < 1) per_sm = 8;
+        slots[G] = (long long)sms * per_sm;
     }
+    return slots[G];
+}
+
+int choose_asplit(const mct_ray_plan* rp, int items) {
+    const int n = items > 0 ? items : 1;
+    const int s1 = adj_split_for((long long)adj_tiles_x(rp->cols) *
+                                     ((rp->rows + AdjShape<1>::PPT * ADJ_WARPS - 1) /
+                                      (AdjShape<1>::PPT * ADJ_WARPS)),
+                                 adj_slots(1), rp);  // single item: the plan's slot count
+    if (!mct_use_pairs(n))
+        return n == 1 ? s1
+                      : adj_split_for((long long)adj_tiles_x(rp->cols) *
+                                          ((rp->rows + AdjShape<1>::PPT * ADJ_WARPS - 1) /
+                                           (AdjShape<1>::PPT * ADJ_WARPS)) * n,
+                                      adj_slots(1), rp);
+    constexpr int TH2 = AdjShape<2>::PPT * ADJ_WARPS;
+    const int s2 = adj_split_for(
+        (long long)adj_tiles_x(rp->cols) * ((rp->rows + TH2 - 1) / TH2) * ((n + 1) / 2),
+        adj_slots(2), rp);
+    return s2 < s1 ? s2 : s1;  // never more slots than the plan holds
+}
+
+template <int G>
+static void launch_adj_g(const AdjArgs& a, int kfoot, int groups, cudaStream_t st) {
+    constexpr int TH = AdjShape<G>::PPT * ADJ_WARPS;
+    dim3 block(ADJ_TW, ADJ_WARPS),
+        grid(adj_tiles_x(a.cols), (a.rows + TH - 1) / TH, groups * a.asplit);
+    switch (kfoot) {
+        case 0: adj_kernel<0, G><<<grid, block, 0, st>>>(a); break;
+        case 1: adj_kernel<1, G><<<grid, block, 0, st>>>(a); break;
+        case 2: adj_kernel<2, G><<<grid, block, 0, st>>>(a); break;
+        default: adj_kernel<3, G><<<grid, block, 0, st>>>(a); break;
+    }
+}
+
+cudaError_t launch_adj(const AdjArgs& a_in, int kfoot, int items, cudaStream_t st) {
+    if (kfoot < 0 || kfoot > 3) return cudaErrorInvalidValue;
+    AdjArgs a = a_in;
+    a.items = items;
+    if (mct_use_pairs(items))
+        launch_adj_g<2>(a, kfoot, (items + 1) / 2, st);
+    else
+        launch_adj_g<1>(a, kfoot, items, st);
     return cudaGetLastError();
 }

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs p) {
         resolve_item(p.sel, item, s_, gate, iter);
         const char* img = p.img_override
                               ? reinterpret_cast<const char*>(p.img_override)
-                              : p.ws + (size_t)item * p.item_bytes + p.off_img;
+                              : p.ws + mct_item_off(item, p.item_bytes, p.pair_block) + p.off_img;
         const int asplit = p.asplit;
         const size_t slot = p.img_slot_bytes;
         // sum of the adjoint's partial-image slots, fixed order (loads four at a time)

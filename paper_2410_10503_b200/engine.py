@@ -135,7 +135,8 @@ class Engine:
         self.dz = None
         items = max_items or max(self.S * self.local, self.S)
         self.max_items = items
-        self.ws = torch.zeros(self.family.item_bytes * items, dtype=torch.uint8, device=dev)
+        self.ws = torch.zeros(int(_lib.load().mct_family_workspace_bytes(self.family.handle, items)),
+                              dtype=torch.uint8, device=dev)
         self.all_gates = torch.arange(self.N, dtype=torch.int32, device=dev)
         self.epoch_ctr = torch.zeros(1, dtype=torch.int32, device=dev)
         self.seq = None

@@ -101,6 +101,10 @@ class _RayPlan:
         self.device = torch.cuda.current_device()
         self.item_bytes = int(L.mct_ray_workspace_bytes(h, 1))
 
+    def workspace_bytes(self, items: int) -> int:
+        """Workspace bytes for launches of up to `items` items (gate-pair blocks)."""
+        return int(_lib.load().mct_ray_workspace_bytes(self.handle, int(items)))
+
     def __del__(self):
         try:
             if self.handle:
@@ -139,7 +143,7 @@ class RayTransform(LinearMap):
         the same stream (calls on other streams get their own buffer).
         """
         torch = _lib.require_cuda()
-        need = self.plan().item_bytes * items
+        need = self.plan().workspace_bytes(items)
         cache = self.__dict__.setdefault("_ws", {})
         key = (torch.cuda.current_device(), _lib.stream_handle())
         ws = cache.get(key)
