@@ -117,7 +117,7 @@ AdjArgs adj_args(const mct_ray_plan* rp, const void* ws) {
     a.img_slot_bytes = rp->img_slot_bytes;
     a.pair_block = rp->pair_block;
     a.off_pdy = rp->off_pdy;
-    a.items = 1;
+    a.item0 = 0;
     a.asplit = 1;
     return a;
 }

@@ -93,11 +93,15 @@ struct mct_ray_plan {
 #define MCT_FWD_ANGLES 4
 #endif
 
-// Launches of >= 2 items run the gate-pair kernels (MCT_PAIRS=0 disables them).
+// Items [0, mct_pair_items(n)) of a launch of n items run the gate-pair kernels
+// (consecutive pairs); an odd last item runs the single-item kernels on its own
+// region.  MCT_PAIRS=0 disables the pair kernels.
 #ifndef MCT_PAIRS
 #define MCT_PAIRS 1
 #endif
-__host__ __device__ __forceinline__ bool mct_use_pairs(int items) { return MCT_PAIRS && items >= 2; }
+__host__ __device__ __forceinline__ int mct_pair_items(int items) {
+    return MCT_PAIRS ? (items & ~1) : 0;
+}
 
 // Byte offset of item `item`'s region and of pair p's region in a workspace.
 __host__ __device__ __forceinline__ size_t mct_item_off(int item, size_t item_bytes,
@@ -110,7 +114,8 @@ __host__ __device__ __forceinline__ size_t mct_pair_off(int pair, size_t item_by
 }
 // Workspace bytes for launches of up to `items` items.
 inline size_t mct_ws_bytes(const mct_ray_plan* p, int items) {
-    return items <= 1 ? p->item_bytes : (size_t)((items + 1) / 2) * p->pair_block;
+    return items <= 1 ? p->item_bytes
+                      : (size_t)(items / 2) * p->pair_block + (size_t)(items & 1) * p->item_bytes;
 }
 
 // --------------------------------------------------------------- warp plan --
@@ -174,7 +179,7 @@ struct PackArgs {
     char* ws;
     size_t item_bytes, off_x, off_xt;
     size_t pair_block, off_px, off_pxt;
-    int paired;              // write the interleaved pair region instead of the item's own
+    int pair_items;          // items below this write the interleaved pair region
     ItemSel sel;
     int N;
     const WarpDesc* warps;   // NULL: identity; with sel.gates NULL: warps[0]
@@ -193,7 +198,7 @@ struct FwdArgs {
     const char* ws;
     size_t item_bytes, off_x, off_xt, off_dy, off_part, off_cnt;
     size_t pair_block, off_px, off_pxt, off_pdy;
-    int items;               // items of the launch (pair mode: the last pair may be half)
+    int item0;               // first item of the launch
     int ksplit;
     int wy, pb;
     ItemSel sel;
@@ -216,7 +221,7 @@ struct AdjArgs {
     const char* ws;
     size_t item_bytes, off_dy, off_img, img_slot_bytes;
     size_t pair_block, off_pdy;
-    int items;
+    int item0;               // first item of the launch
     int asplit;
 };
 

@@ -51,13 +51,14 @@ __global__ void __launch_bounds__(THREADS, MINB) pack_kernel(PackArgs p) {
 
     // own region: element e at X[e]; pair mode: the pair region, element e of this
     // item at X[2e + (item & 1)] (float2 halves of the interleaved float4)
-    char* base = p.paired ? p.ws + mct_pair_off(item >> 1, p.item_bytes, p.pair_block)
-                          : p.ws + mct_item_off(item, p.item_bytes, p.pair_block);
-    const int es = p.paired ? 2 : 1;
-    float2* X = reinterpret_cast<float2*>(base + (p.paired ? p.off_px : p.off_x)) + es * MCT_PADX +
-                (p.paired ? (item & 1) : 0);
-    float2* XT = reinterpret_cast<float2*>(base + (p.paired ? p.off_pxt : p.off_xt)) +
-                 es * MCT_PADX + (p.paired ? (item & 1) : 0);
+    const bool paired = item < p.pair_items;
+    char* base = paired ? p.ws + mct_pair_off(item >> 1, p.item_bytes, p.pair_block)
+                        : p.ws + mct_item_off(item, p.item_bytes, p.pair_block);
+    const int es = paired ? 2 : 1;
+    float2* X = reinterpret_cast<float2*>(base + (paired ? p.off_px : p.off_x)) + es * MCT_PADX +
+                (paired ? (item & 1) : 0);
+    float2* XT = reinterpret_cast<float2*>(base + (paired ? p.off_pxt : p.off_xt)) +
+                 es * MCT_PADX + (paired ? (item & 1) : 0);
 
     const int c0 = blockIdx.x * T, r0 = blockIdx.y * T;
     const int tid = threadIdx.x;
@@ -104,16 +105,18 @@ __global__ void __launch_bounds__(THREADS, MINB) pack_kernel(PackArgs p) {
 // the item's half of its pair region), pre-scaled by the angle's step length
 // (A^* then only needs the tent weights).
 __global__ void pad_sino_kernel(const float* __restrict__ sino, const AdjAngle* __restrict__ ang,
-                                char* ws, size_t item_bytes, size_t pair_block, size_t off_dy,
-                                int A, int B, int wy, int pb, int paired) {
+                                char* ws, size_t item_bytes, size_t pair_block, size_t off_dy1,
+                                size_t off_dy2,
+                                int A, int B, int wy, int pb, int pair_items) {
     const int item = blockIdx.z;
+    const bool paired = item < pair_items;
     const int a = blockIdx.y;
     const float step = ang[a].step;
     const int G = paired ? 2 : 1;
     float* DY = reinterpret_cast<float*>(
                     ws + (paired ? mct_pair_off(item >> 1, item_bytes, pair_block)
                                  : mct_item_off(item, item_bytes, pair_block)) +
-                    off_dy) +
+                    (paired ? off_dy2 : off_dy1)) +
                 (paired ? 2 * (item & 1) : 0);
     const float* s = sino + ((long long)item * A + a) * B;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x) {
@@ -159,13 +162,15 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
 #define FWD_MIN_BLOCKS 12         // 12 x 4 warps resident: 40 registers for 8 loads in flight
 #endif
 
-// Single-item K2 (one gate per block): kept as its own kernel; the G = 1
-// instantiation of the generic kernel below schedules 20 % slower (ptxas).
+// Single-item K2 (one gate per block).  Kept as its own kernel: the G = 1
+// instantiation of the gate-pair kernel below gets a ptxas schedule that runs
+// the single-gate SPDHG K2 20 % slower.  Both kernels are schedule-sensitive:
+// check `-Xptxas -v` (no spills) and the sweep tools after editing either.
 template <int MODE, int LPT>
 __global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel1(FwdArgs p) {
     const int ks = p.ksplit;
-    const int item = blockIdx.z / ks;
-    const int part = blockIdx.z - item * ks;
+    const int item = p.item0 + (int)blockIdx.z / ks;
+    const int part = (int)blockIdx.z % ks;
     // LPT (single-gate launches): grid (angle groups, bin tiles by distance rank, parts): every angle group's
     // central tiles (the longest rays) are dispatched before any edge tile, so the
     // last, partial wave holds the shortest blocks
@@ -369,9 +374,6 @@ __device__ __forceinline__ float td(const float4& v, int h) { return h ? v.w : v
 #ifndef FWD_MIN_BLOCKS2
 #define FWD_MIN_BLOCKS2 8
 #endif
-#ifndef FWD_PAIR_ORDER
-#define FWD_PAIR_ORDER 1  // 1: gate-pair K2 consumes sample by sample (see the core loop)
-#endif
 
 // G = 2: one warp walks the rays of two items (a gate pair) at once; every
 // per-item sum is accumulated exactly as with G = 1 (bitwise equal results).
@@ -402,7 +404,7 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, G == 1 ? FWD_MIN_BLOCKS : FWD
     const bool active = warp_on && j < p.B;
     const int jj = active ? j : p.B - 1;  // idle lanes shadow the last bin (no store)
     const RayAngle ra = p.ang[a];
-    const int item0 = G * group;
+    const int item0 = G * group;  // pair launches start at item 0
     const char* base0 = p.ws + mct_item_off(item0, p.item_bytes, p.pair_block);  // counters
     const char* tb = G == 1 ? base0 : p.ws + mct_pair_off(group, p.item_bytes, p.pair_block);
     const int cd = ra.cols_dom;
@@ -494,33 +496,17 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, G == 1 ? FWD_MIN_BLOCKS : FWD
                 flo = lo8[7];
                 fhi = hi8[7];
                 fx_add(flo, fhi, ilo, ihi);
-                // consumption order steers ptxas' schedule under the register cap:
-                // values of a half-trip first, then its differences (G = 1: 20 %
-                // faster single-gate K2 than sample-by-sample consumption)
-                if (G == 1 || FWD_PAIR_ORDER == 0) {
 #pragma unroll
-                    for (int hb = 0; hb < 2; ++hb) {
+                for (int hb = 0; hb < 2; ++hb) {
 #pragma unroll
-                        for (int h = 0; h < G; ++h)
+                    for (int h = 0; h < G; ++h)
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) s[h][q] += tv(v[4 * hb + q], h);
+                        for (int q = 0; q < 4; ++q) s[h][q] += tv(v[4 * hb + q], h);
 #pragma unroll
-                        for (int h = 0; h < G; ++h)
+                    for (int h = 0; h < G; ++h)
 #pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                t[h][q] = fmaf((float)(lo8[4 * hb + q] >> 8), td(v[4 * hb + q], h),
-                                               t[h][q]);
-                    }
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const float f = (float)(lo8[u] >> 8);
-#pragma unroll
-                        for (int h = 0; h < G; ++h) {
-                            s[h][u & 3] += tv(v[u], h);
-                            t[h][u & 3] = fmaf(f, td(v[u], h), t[h][u & 3]);
-                        }
-                    }
+                        for (int q = 0; q < 4; ++q)
+                            t[h][q] = fmaf((float)(lo8[4 * hb + q] >> 8), td(v[4 * hb + q], h), t[h][q]);
                 }
             }
             for (; kk <= kend; ++kk) {
@@ -554,8 +540,7 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, G == 1 ? FWD_MIN_BLOCKS : FWD
 #pragma unroll
         for (int h = 0; h < G; ++h) tot[h] = dacc[h] + (double)ea[h];
     }
-    // items of this block (the second half of a last, odd pair is a dummy)
-    const int nval = G == 1 ? 1 : min(G, p.items - item0);
+    constexpr int nval = G;
     double sum[G];
 #pragma unroll
     for (int h = 0; h < G; ++h) sum[h] = tot[h];
@@ -749,8 +734,13 @@ __device__ __forceinline__ void adj_tap1(const typename TapVec<G>::T* __restrict
 #define ADJ_MIN_BLOCKS2 6
 #endif
 template <int G> struct AdjShape;
-template <> struct AdjShape<1> { static constexpr int PPT = ADJ_PPT, MINB = ADJ_MIN_BLOCKS; };
-template <> struct AdjShape<2> { static constexpr int PPT = ADJ_PPT2, MINB = ADJ_MIN_BLOCKS2; };
+#ifndef ADJ_TU2
+#define ADJ_TU2 4      // unroll of the angle-pair loop (gate-pair kernel)
+#endif
+template <> struct AdjShape<1> { static constexpr int PPT = ADJ_PPT, MINB = ADJ_MIN_BLOCKS, TU = 2; };
+template <> struct AdjShape<2> {
+    static constexpr int PPT = ADJ_PPT2, MINB = ADJ_MIN_BLOCKS2, TU = ADJ_TU2;
+};
 
 // G = 2: a thread owns its pixels in the two items of a gate pair; the bins and
 // tent weights are computed once and applied to both items' rows (one 16-byte
@@ -781,9 +771,9 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
     const int cmc = p.cols - 1 - (c0 + txc);                 // (clamped) mirror column
     const double u0 = (double)r0 - 0.5 * (double)(p.rows - 1);
     const double v0 = (double)c0 - 0.5 * (double)(p.cols - 1);
-    const int item0 = G * group;
+    const int item0 = p.item0 + G * group;  // G = 2: item0 is even
     const char* tb = G == 1 ? p.ws + mct_item_off(item0, p.item_bytes, p.pair_block)
-                            : p.ws + mct_pair_off(group, p.item_bytes, p.pair_block);
+                            : p.ws + mct_pair_off(item0 >> 1, p.item_bytes, p.pair_block);
     const V* __restrict__ DY2 = reinterpret_cast<const V*>(tb + (G == 1 ? p.off_dy : p.off_pdy));
     const long long row_off = (long long)(threadIdx.y * PPT);
 
@@ -843,7 +833,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
         for (int m = 0; m < PPT; ++m)
 #pragma unroll
             for (int h = 0; h < G; ++h) acc[m][h] = accm[m][h] = 0.0f;
-#pragma unroll 2
+#pragma unroll (AdjShape<G>::TU)
         for (int t = 0; t < cnt; ++t) {
             const longlong2 T2 = s_t[t];
             const int4 U = s_u[t];
@@ -876,7 +866,6 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
     if (c >= ncl) return;
 #pragma unroll
     for (int h = 0; h < G; ++h) {
-        if (G > 1 && item0 + h >= p.items) break;  // dummy half of a last, odd pair
         float* IMG = reinterpret_cast<float*>(
             const_cast<char*>(p.ws) + mct_item_off(item0 + h, p.item_bytes, p.pair_block) +
             p.off_img + (size_t)split * p.img_slot_bytes);
@@ -905,7 +894,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
 #endif
 cudaError_t launch_pack(const PackArgs& a_in, int items, cudaStream_t st) {
     PackArgs a = a_in;
-    a.paired = mct_use_pairs(items) ? 1 : 0;
+    a.pair_items = mct_pair_items(items);
     if (items <= PACK_SMALL_ITEMS) {  // few gates: small tiles, one halo element per thread
         dim3 grid((a.cols + 15) / 16, (a.rows + 15) / 16, items);
         pack_kernel<16, 320, PACK16_MINB><<<grid, 320, 0, st>>>(a);
@@ -919,10 +908,9 @@ cudaError_t launch_pack(const PackArgs& a_in, int items, cudaStream_t st) {
 cudaError_t launch_pad_sino(const float* sino, const mct_ray_plan* rp, char* ws, int items,
                             cudaStream_t st) {
     dim3 block(256), grid((rp->B + 255) / 256, rp->A, items);
-    const bool paired = mct_use_pairs(items);
     pad_sino_kernel<<<grid, block, 0, st>>>(sino, rp->d_adj, ws, rp->item_bytes, rp->pair_block,
-                                            paired ? rp->off_pdy : rp->off_dy, rp->A, rp->B,
-                                            rp->wy, rp->pb, paired ? 1 : 0);
+                                            rp->off_dy, rp->off_pdy, rp->A, rp->B, rp->wy, rp->pb,
+                                            mct_pair_items(items));
     return cudaGetLastError();
 }
 
@@ -970,22 +958,26 @@ static void fwd_prefer_l1() {
 cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st) {
     fwd_prefer_l1();
     FwdArgs a = a_in;
-    a.items = items;
     dim3 block(32, FWD_ANGLES);
     const unsigned ntile = (a.B + 31) / 32, ngroup = (a.A + FWD_ANGLES - 1) / FWD_ANGLES;
-    if (mct_use_pairs(items)) {  // gate pairs (bins fastest: L2 locality across pairs)
-        dim3 grid(ntile, ngroup, ((items + 1) / 2) * a.ksplit);
+    const int np = mct_pair_items(items);
+    if (np > 0) {  // gate pairs (bins fastest: L2 locality across pairs)
+        a.item0 = 0;
+        dim3 grid(ntile, ngroup, (np / 2) * a.ksplit);
         if (mode == 0)
             fwd_kernel<0, 0, 2><<<grid, block, 0, st>>>(a);
         else
             fwd_kernel<1, 0, 2><<<grid, block, 0, st>>>(a);
-        return cudaGetLastError();
+        if (np == items) return cudaGetLastError();
     }
-    // one single-gate item: longest-rays-first dispatch order (LPT) shrinks the
-    // last partial wave; with many items (C5 batch) the item-major order keeps
-    // better L2 locality.  Same arithmetic either way (block order only).
-    const bool lpt = a.ksplit > 1 && items == 1;
-    dim3 grid(lpt ? ngroup : ntile, lpt ? ntile : ngroup, items * a.ksplit);
+    // single items (an odd last item after the pairs).  One single-gate item:
+    // longest-rays-first dispatch order (LPT) shrinks the last partial wave; with
+    // many items the item-major order keeps better L2 locality.  Same arithmetic
+    // either way (block order only).
+    a.item0 = np;
+    const int rest = items - np;
+    const bool lpt = a.ksplit > 1 && rest == 1;
+    dim3 grid(lpt ? ngroup : ntile, lpt ? ntile : ngroup, rest * a.ksplit);
     if (lpt) {
         if (mode == 0)
             fwd_kernel1<0, 1><<<grid, block, 0, st>>>(a);
@@ -1052,20 +1044,13 @@ static long long adj_slots(int G) {
 
 int choose_asplit(const mct_ray_plan* rp, int items) {
     const int n = items > 0 ? items : 1;
-    const int s1 = adj_split_for((long long)adj_tiles_x(rp->cols) *
-                                     ((rp->rows + AdjShape<1>::PPT * ADJ_WARPS - 1) /
-                                      (AdjShape<1>::PPT * ADJ_WARPS)),
-                                 adj_slots(1), rp);  // single item: the plan's slot count
-    if (!mct_use_pairs(n))
-        return n == 1 ? s1
-                      : adj_split_for((long long)adj_tiles_x(rp->cols) *
-                                          ((rp->rows + AdjShape<1>::PPT * ADJ_WARPS - 1) /
-                                           (AdjShape<1>::PPT * ADJ_WARPS)) * n,
-                                      adj_slots(1), rp);
-    constexpr int TH2 = AdjShape<2>::PPT * ADJ_WARPS;
-    const int s2 = adj_split_for(
-        (long long)adj_tiles_x(rp->cols) * ((rp->rows + TH2 - 1) / TH2) * ((n + 1) / 2),
-        adj_slots(2), rp);
+    constexpr int TH1 = AdjShape<1>::PPT * ADJ_WARPS, TH2 = AdjShape<2>::PPT * ADJ_WARPS;
+    const long long tiles1 = (long long)adj_tiles_x(rp->cols) * ((rp->rows + TH1 - 1) / TH1);
+    const int s1 = adj_split_for(tiles1, adj_slots(1), rp);  // single item: the plan's slot count
+    const int np = mct_pair_items(n);
+    if (np == 0) return n == 1 ? s1 : adj_split_for(tiles1 * n, adj_slots(1), rp);
+    const long long tiles2 = (long long)adj_tiles_x(rp->cols) * ((rp->rows + TH2 - 1) / TH2);
+    const int s2 = adj_split_for(tiles2 * (np / 2 + (n - np)), adj_slots(2), rp);
     return s2 < s1 ? s2 : s1;  // never more slots than the plan holds
 }
 
@@ -1082,13 +1067,19 @@ static void launch_adj_g(const AdjArgs& a, int kfoot, int groups, cudaStream_t s
     }
 }
 
+// Pairs first, then an odd last item on its own; both launches use the caller's
+// angle split (K4 sums the same number of partial slots for every item).
 cudaError_t launch_adj(const AdjArgs& a_in, int kfoot, int items, cudaStream_t st) {
     if (kfoot < 0 || kfoot > 3) return cudaErrorInvalidValue;
     AdjArgs a = a_in;
-    a.items = items;
-    if (mct_use_pairs(items))
-        launch_adj_g<2>(a, kfoot, (items + 1) / 2, st);
-    else
-        launch_adj_g<1>(a, kfoot, items, st);
+    const int np = mct_pair_items(items);
+    if (np > 0) {
+        a.item0 = 0;
+        launch_adj_g<2>(a, kfoot, np / 2, st);
+    }
+    if (items > np) {
+        a.item0 = np;
+        launch_adj_g<1>(a, kfoot, items - np, st);
+    }
     return cudaGetLastError();
 }
