@@ -113,18 +113,24 @@ def test_linearity_and_zero(m):
         m.adjoint(geom, np.zeros((11, 30)))
 
 
-def test_batched_forward_equals_single(m):
+@pytest.mark.parametrize("batch", [2, 3, 4, 5])
+@pytest.mark.parametrize("shape", [(48, 40, 30, 70, 1.0), (33, 64, 31, 80, 0.9)])
+def test_batched_forward_equals_single(m, batch, shape):
+    """Batches run the gate-pair kernels (items 2p, 2p+1 share one walk / one set
+    of tent weights, an odd last item the single-item kernels): every item's
+    result is bitwise the single-item one (with <= 16 angle pairs the A^* angle
+    split is 1 for any launch)."""
     import torch
 
-    geom = m.Geometry(48, 40, 30, 70, 1.0)
+    geom = m.Geometry(*shape)
     op = m.RayTransform(geom)
-    x = torch.randn(3, 48, 40, device="cuda")
+    x = torch.randn(batch, geom.rows, geom.cols, device="cuda")
     yb = op.forward_batch(x)
-    for i in range(3):
+    for i in range(batch):
         assert torch.equal(yb[i], op.apply(x[i]))
-    y = torch.randn(3, 30, 70, device="cuda")
+    y = torch.randn(batch, geom.num_angles, geom.num_bins, device="cuda")
     xb = op.adjoint_batch(y)
-    for i in range(3):
+    for i in range(batch):
         assert torch.equal(xb[i], op.adjoint_apply(y[i]))
 
 
