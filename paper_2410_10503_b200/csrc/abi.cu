@@ -243,14 +243,16 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     p->pb = pb;
     p->wy = num_bins + 2 * pb;
     size_t off = 0;
-    // pair-packed layouts: element i holds (v[i], v[i+1]) so one 8-byte load
-    // fetches both interpolation taps
+    // pair-packed layouts (float2 (v[i], v[i+1] - v[i]): one load fetches both
+    // interpolation taps), two per float4 element: the item and its column
+    // mirror (X, XT), angles q and A-q (DY rows 1 .. (A-1)/2; row 0 holds the
+    // self-paired angles 0 and A/2) -- see mct_internal.cuh
     p->off_x = off;
-    off += align256((size_t)rows * p->wx * sizeof(float2));
+    off += align256((size_t)rows * p->wx * sizeof(float4));
     p->off_xt = off;
-    off += align256((size_t)cols * p->wxt * sizeof(float2));
+    off += align256((size_t)cols * p->wxt * sizeof(float4));
     p->off_dy = off;
-    off += align256((size_t)num_angles * p->wy * sizeof(float2));
+    off += align256((size_t)(num_angles / 2 + 1) * p->wy * sizeof(float4));
     p->off_img = off;
     p->img_slot_bytes = align256((size_t)rows * cols * sizeof(float));
     // A^* partial-image slots: the largest angle split any launch of this plan

@@ -10,6 +10,20 @@
 
 namespace {
 
+// Angle slots of a single-item (mirror) launch: slot s < nsingle is a
+// self-paired angle (0, and A/2 for even A), slot s >= nsingle the mirror pair
+// (q, A-q), q = s - nsingle + 1.  Sinogram row / float2 slot of angle a in the
+// mirror DY layout: pairs (q, h), self-paired angles (0, s).
+__host__ __device__ __forceinline__ int mir_nsingle(int A) { return (A % 2 == 0) ? 2 : 1; }
+__host__ __device__ __forceinline__ int mir_slots(int A) { return mir_nsingle(A) + (A - 1) / 2; }
+__device__ __forceinline__ void mir_row_slot(int a, int A, int& row, int& slot) {
+    const int np = (A - 1) / 2;
+    if (a == 0) { row = 0; slot = 0; }
+    else if (a <= np) { row = a; slot = 0; }
+    else if (2 * a == A) { row = 0; slot = 1; }
+    else { row = A - a; slot = 1; }
+}
+
 // ---------------------------------------------------------------------------
 // K1 / pack: W = D_g(x_new), x_new = prox_g(x - tau*zbar) (or x_new = x), written
 // into the padded row-major X2 and transposed XT2 of the item workspace in the
@@ -23,8 +37,8 @@ namespace {
 // ---------------------------------------------------------------------------
 template <int T, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) pack_kernel(PackArgs p) {
-    constexpr int H = T + 1;
-    __shared__ float tile[H][H + 1];
+    constexpr int HR = T + 1, HC = T + 2;  // rows r0 .. r0+T, cols c0-1 .. c0+T
+    __shared__ float tile[HR][HC + 1];
     const int item = blockIdx.z;
     int slice, gate, iter;
     resolve_item(p.sel, item, slice, gate, iter);
@@ -49,28 +63,28 @@ __global__ void __launch_bounds__(THREADS, MINB) pack_kernel(PackArgs p) {
         return v;
     };
 
-    // own region: element e at X[e]; pair mode: the pair region, element e of this
-    // item at X[2e + (item & 1)] (float2 halves of the interleaved float4)
+    // Both layouts hold float4 elements = two float2 slots (value, forward
+    // difference).  Pair mode: slot (item & 1) of the pair region holds this
+    // item.  Single-item (mirror) mode: slot 0 holds W, slot 1 the column mirror
+    // Wm[r][c] = W[r][cols-1-c] (X) / XT[cols-1-c] (XT) of the item's own region.
     const bool paired = item < p.pair_items;
     char* base = paired ? p.ws + mct_pair_off(item >> 1, p.item_bytes, p.pair_block)
                         : p.ws + mct_item_off(item, p.item_bytes, p.pair_block);
-    const int es = paired ? 2 : 1;
-    float2* X = reinterpret_cast<float2*>(base + (paired ? p.off_px : p.off_x)) + es * MCT_PADX +
-                (paired ? (item & 1) : 0);
-    float2* XT = reinterpret_cast<float2*>(base + (paired ? p.off_pxt : p.off_xt)) +
-                 es * MCT_PADX + (paired ? (item & 1) : 0);
+    const int s0 = paired ? (item & 1) : 0;
+    float2* X = reinterpret_cast<float2*>(base + (paired ? p.off_px : p.off_x)) + 2 * MCT_PADX;
+    float2* XT = reinterpret_cast<float2*>(base + (paired ? p.off_pxt : p.off_xt)) + 2 * MCT_PADX;
 
     const int c0 = blockIdx.x * T, r0 = blockIdx.y * T;
     const int tid = threadIdx.x;
     const bool writer = prox && k_in_slice == 0 && p.x_next != nullptr;
     bool bad = false;
-    for (int idx = tid; idx < H * H; idx += THREADS) {
-        const int i = idx / H, jj = idx - i * H;
-        const int r = r0 + i, c = c0 + jj;
+    for (int idx = tid; idx < HR * HC; idx += THREADS) {
+        const int i = idx / HC, jj = idx - i * HC;
+        const int r = r0 + i, c = c0 - 1 + jj;
         float w = 0.0f;
-        if (r < rows && c < cols) {
+        if (r < rows && c >= 0 && c < cols) {
             w = ident ? xnew(r, c) : warp_apply_at(wd, r, c, xnew);
-            if (writer && i < T && jj < T) {
+            if (writer && i < T && jj >= 1 && jj <= T) {
                 const float xn = xnew(r, c);
                 p.x_next[(long long)slice * p.x_slice_stride + (long long)r * cols + c] = xn;
                 bad |= !isfinite(xn);
@@ -87,43 +101,54 @@ __global__ void __launch_bounds__(THREADS, MINB) pack_kernel(PackArgs p) {
         const int i = o / T, tx = o - i * T;
         const int r = r0 + i, c = c0 + tx;
         if (r < rows && c < cols) {
-            const float w = tile[i][tx];
-            X[es * ((long long)r * p.wx + c)] = make_float2(w, tile[i][tx + 1] - w);
-            if (c == 0) X[es * ((long long)r * p.wx - 1)] = make_float2(0.0f, w);
+            const float w = tile[i][tx + 1];
+            const long long row = (long long)r * p.wx;
+            X[2 * (row + c) + s0] = make_float2(w, tile[i][tx + 2] - w);
+            if (c == 0) X[2 * (row - 1) + s0] = make_float2(0.0f, w);
+            if (!paired) {  // mirror slot: element cols-1-c pairs W[c] with W[c-1]
+                X[2 * (row + cols - 1 - c) + 1] = make_float2(w, tile[i][tx] - w);
+                if (c == cols - 1) X[2 * (row - 1) + 1] = make_float2(0.0f, w);
+            }
         }
         // transposed: element (c, r) pairs W[r][c] with W[r+1][c]
         const int ct = c0 + i, rt = r0 + tx;
         if (rt < rows && ct < cols) {
-            const float w = tile[tx][i];
-            XT[es * ((long long)ct * p.wxt + rt)] = make_float2(w, tile[tx + 1][i] - w);
-            if (rt == 0) XT[es * ((long long)ct * p.wxt - 1)] = make_float2(0.0f, w);
+            const float w = tile[tx][i + 1];
+            const float2 v = make_float2(w, tile[tx + 1][i + 1] - w);
+            XT[2 * ((long long)ct * p.wxt + rt) + s0] = v;
+            if (rt == 0) XT[2 * ((long long)ct * p.wxt - 1) + s0] = make_float2(0.0f, w);
+            if (!paired) {  // mirror slot: row cols-1-ct of the transposed layout
+                const long long rowm = (long long)(cols - 1 - ct) * p.wxt;
+                XT[2 * (rowm + rt) + 1] = v;
+                if (rt == 0) XT[2 * (rowm - 1) + 1] = make_float2(0.0f, w);
+            }
         }
     }
 }
 
-// Copy a plain (A, B) sinogram into the pair-packed padded DY2 of each item (or
-// the item's half of its pair region), pre-scaled by the angle's step length
-// (A^* then only needs the tent weights).
+// Copy a plain (A, B) sinogram into the padded float4 DY layout of each item,
+// pre-scaled by the angle's step length (A^* then only needs the tent weights):
+// paired items into their slot of the pair region (row a), single items into
+// the mirror layout of their own region (row / slot of mir_row_slot).
 __global__ void pad_sino_kernel(const float* __restrict__ sino, const AdjAngle* __restrict__ ang,
                                 char* ws, size_t item_bytes, size_t pair_block, size_t off_dy1,
-                                size_t off_dy2,
-                                int A, int B, int wy, int pb, int pair_items) {
+                                size_t off_dy2, int A, int B, int wy, int pb, int pair_items) {
     const int item = blockIdx.z;
     const bool paired = item < pair_items;
     const int a = blockIdx.y;
     const float step = ang[a].step;
-    const int G = paired ? 2 : 1;
+    int row = a, slot = item & 1;
+    if (!paired) mir_row_slot(a, A, row, slot);
     float* DY = reinterpret_cast<float*>(
                     ws + (paired ? mct_pair_off(item >> 1, item_bytes, pair_block)
                                  : mct_item_off(item, item_bytes, pair_block)) +
-                    (paired ? off_dy2 : off_dy1)) +
-                (paired ? 2 * (item & 1) : 0);
+                    (paired ? off_dy2 : off_dy1)) + 2 * slot;
     const float* s = sino + ((long long)item * A + a) * B;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x) {
-        const long long e = 2 * G * ((long long)a * wy + pb + j);
+        const long long e = 4 * ((long long)row * wy + pb + j);
         const float v = s[j] * step;
         DY[e] = v;
-        DY[e - 2 * G + 1] = v;
+        DY[e - 3] = v;
     }
 }
 
@@ -162,227 +187,34 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
 #define FWD_MIN_BLOCKS 12         // 12 x 4 warps resident: 40 registers for 8 loads in flight
 #endif
 
-// Single-item K2 (one gate per block).  Kept as its own kernel: the G = 1
-// instantiation of the gate-pair kernel below gets a ptxas schedule that runs
-// the single-gate SPDHG K2 20 % slower.  Both kernels are schedule-sensitive:
-// check `-Xptxas -v` (no spills) and the sweep tools after editing either.
-template <int MODE, int LPT>
-__global__ void __launch_bounds__(32 * FWD_ANGLES, FWD_MIN_BLOCKS) fwd_kernel1(FwdArgs p) {
-    const int ks = p.ksplit;
-    const int item = p.item0 + (int)blockIdx.z / ks;
-    const int part = (int)blockIdx.z % ks;
-    // LPT (single-gate launches): grid (angle groups, bin tiles by distance rank, parts): every angle group's
-    // central tiles (the longest rays) are dispatched before any edge tile, so the
-    // last, partial wave holds the shortest blocks
-    // (multi-gate launches keep bins fastest: better L2 locality across gates)
-    const int btile = LPT ? [&] {
-        const int ntile = gridDim.y, c = ntile / 2, k = blockIdx.y;
-        if (k == 0) return c;
-        const int jr = k - 1, below = c, above = ntile - 1 - c;
-        const int pairs = below < above ? below : above;
-        if (jr < 2 * pairs) return (jr & 1) ? c + 1 + (jr >> 1) : c - 1 - (jr >> 1);
-        const int r = jr - 2 * pairs;
-        return below > above ? c - 1 - pairs - r : c + 1 + pairs + r;
-    }() : (int)blockIdx.x;
-    const int a_raw = (LPT ? blockIdx.x : blockIdx.y) * FWD_ANGLES + threadIdx.y;
-    const bool warp_on = a_raw < p.A;        // warp-uniform; no early exit (block syncs below)
-    const int a = warp_on ? a_raw : p.A - 1;
-    const int j = btile * 32 + threadIdx.x;
-    const bool active = warp_on && j < p.B;
-    const int jj = active ? j : p.B - 1;  // idle lanes shadow the last bin (no store)
-    const RayAngle ra = p.ang[a];
-    const char* base = p.ws + mct_item_off(item, p.item_bytes, p.pair_block);
-    const int cd = ra.cols_dom;
-    // tap index = hi(fx) >= 0: the row pad is folded into fx so the address is one
-    // unsigned 32x64 multiply-add
-    const float2* __restrict__ X2 =
-        reinterpret_cast<const float2*>(base + (cd ? p.off_xt : p.off_x));
-    const int stride = cd ? p.wxt : p.wx;
-    const int nmaj = cd ? p.cols : p.rows;
-    const int lim = cd ? p.rows : p.cols;
-
-    // per-ray range of dominant-axis samples that can have a tap inside the grid
-    const double sj = ((double)jj - p.jmid) * p.sp;
-    const double c0 = ra.P * sj + ra.Q;
-    int lo = nmaj, hi = -1;
-    if (ra.slope == 0.0) {
-        if (c0 > -1.0 && c0 < (double)lim) { lo = 0; hi = nmaj - 1; }
-    } else {
-        const double ka = (-1.0 - c0) / ra.slope, kb = ((double)lim - c0) / ra.slope;
-        const double top = (double)nmaj + 2.0;
-        const double kmin = fmin(fmax(fmin(ka, kb), -2.0), top);
-        const double kmax = fmin(fmax(fmax(ka, kb), -2.0), top);
-        lo = max(0, (int)floor(kmin));
-        hi = min(nmaj - 1, (int)ceil(kmax));
-    }
-    int wlo = __reduce_min_sync(0xffffffffu, lo);  // union of the warp's ranges
-    int whi = __reduce_max_sync(0xffffffffu, hi);
-    int clo = __reduce_max_sync(0xffffffffu, lo);        // common core
-    int chi = __reduce_min_sync(0xffffffffu, hi);
-    // this block's share of the walk: part `part` of ks equal pieces
-    const int wlen = whi - wlo + 1;
-    const int k_lo = wlo + (int)((long long)wlen * part / ks);
-    const int k_hi = wlo + (int)((long long)wlen * (part + 1) / ks) - 1;
-    wlo = k_lo;
-    whi = k_hi;
-    clo = max(clo, k_lo);
-    chi = min(chi, k_hi);
-    double tot = 0.0;
-    if (warp_on && wlo <= whi) {
-        if (clo > chi) { clo = whi + 1; chi = whi; }     // no common core: all edge
-        const long long inc64 = ra.slope_fx + ((long long)stride << 32);
-        const unsigned ilo = (unsigned)inc64, ihi = (unsigned)(inc64 >> 32);
-        const long long fx0 = __double2ll_rn((c0 + (double)wlo * ra.slope) * FX_ONE) +
-                              ((long long)(wlo * stride + MCT_PADX) << 32);
-        unsigned flo = (unsigned)fx0, fhi = (unsigned)(fx0 >> 32);
-        int rowoff = wlo * stride + MCT_PADX;
-        const unsigned lim1 = (unsigned)(lim + 1);
-        double dacc = 0.0;
-        float ea = 0.0f;  // ragged-edge samples (predicated on the tap range)
-        int k = wlo;
-        for (; k < clo; ++k) {
-            const int i0 = (int)fhi - rowoff;
-            if ((unsigned)(i0 + 1) < lim1) {
-                const float2 v = __ldg(X2 + fhi);
-                ea += fmaf((float)(flo >> 8) * INV_2_24, v.y, v.x);
-            }
-            fx_add(flo, fhi, ilo, ihi);
-            rowoff += stride;
-        }
-        // core: every lane's taps are inside the padded row (pads read zero)
-        for (int kc = k; kc <= chi; kc += 64) {
-            const int kend = min(chi, kc + 63);
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // sum of v0
-            float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;  // sum of frac*2^24*(x[i+1] - x[i])
-            int kk = kc;
-            // 8 samples per trip: all 8 loads are issued before the first use
-            for (; kk + 7 <= kend; kk += 8) {
-                unsigned lo8[8], hi8[8];
-                lo8[0] = flo;
-                hi8[0] = fhi;
-#pragma unroll
-                for (int u = 1; u < 8; ++u) {
-                    lo8[u] = lo8[u - 1];
-                    hi8[u] = hi8[u - 1];
-                    fx_add(lo8[u], hi8[u], ilo, ihi);
-                }
-                float2 v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = __ldg(X2 + hi8[u]);
-                flo = lo8[7];
-                fhi = hi8[7];
-                fx_add(flo, fhi, ilo, ihi);
-                s0 += v[0].x; s1 += v[1].x; s2 += v[2].x; s3 += v[3].x;
-                t0 = fmaf((float)(lo8[0] >> 8), v[0].y, t0);
-                t1 = fmaf((float)(lo8[1] >> 8), v[1].y, t1);
-                t2 = fmaf((float)(lo8[2] >> 8), v[2].y, t2);
-                t3 = fmaf((float)(lo8[3] >> 8), v[3].y, t3);
-                s0 += v[4].x; s1 += v[5].x; s2 += v[6].x; s3 += v[7].x;
-                t0 = fmaf((float)(lo8[4] >> 8), v[4].y, t0);
-                t1 = fmaf((float)(lo8[5] >> 8), v[5].y, t1);
-                t2 = fmaf((float)(lo8[6] >> 8), v[6].y, t2);
-                t3 = fmaf((float)(lo8[7] >> 8), v[7].y, t3);
-            }
-            for (; kk <= kend; ++kk) {
-                const float2 v0 = __ldg(X2 + fhi);
-                s0 += v0.x;
-                t0 = fmaf((float)(flo >> 8), v0.y, t0);
-                fx_add(flo, fhi, ilo, ihi);
-            }
-            dacc += (double)((s0 + s1) + (s2 + s3)) +
-                    (double)((t0 + t1) + (t2 + t3)) * (double)INV_2_24;
-            k = kend + 1;
-        }
-        rowoff = k * stride + MCT_PADX;
-        for (; k <= whi; ++k) {
-            const int i0 = (int)fhi - rowoff;
-            if ((unsigned)(i0 + 1) < lim1) {
-                const float2 v = __ldg(X2 + fhi);
-                ea += fmaf((float)(flo >> 8) * INV_2_24, v.y, v.x);
-            }
-            fx_add(flo, fhi, ilo, ihi);
-            rowoff += stride;
-        }
-        tot = dacc + (double)ea;
-    }
-    double sum = tot;
-    if (ks > 1) {
-        // combine the parts: the last block of this tile to arrive sums them in order
-        double* PART = reinterpret_cast<double*>(const_cast<char*>(base) + p.off_part);
-        if (active) PART[((long long)part * p.A + a) * p.B + j] = tot;
-        __shared__ int s_last;
-        __syncthreads();
-        if (threadIdx.x == 0 && threadIdx.y == 0) {
-            int* cnt = reinterpret_cast<int*>(const_cast<char*>(base) + p.off_cnt) +
-                       blockIdx.y * gridDim.x + blockIdx.x;
-#if FWD_ACQREL
-            // release: the block's PART stores (ordered before by the barrier);
-            // acquire: the other parts' stores, for the last block to arrive
-            int prev;
-            asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
-                         : "=r"(prev) : "l"(cnt) : "memory");
-#else
-            __threadfence();
-            const int prev = atomicAdd(cnt, 1);
+#ifndef FWD_MIN_BLOCKS2
+#define FWD_MIN_BLOCKS2 8         // gate pairs: 8 x 4 warps resident, 64 registers
 #endif
-            s_last = (prev == ks - 1);
-            if (s_last) *cnt = 0;  // every part has arrived: re-arm for the next launch
-        }
-        __syncthreads();
-        if (!s_last || !active) return;
-#if !FWD_ACQREL
-        __threadfence();
+#ifndef FWD_MIN_BLOCKS_M
+#define FWD_MIN_BLOCKS_M 7        // single-item mirror walks (72 registers, no spills)
 #endif
-        sum = 0.0;
-        for (int q = 0; q < ks; ++q) sum += __ldcg(PART + ((long long)q * p.A + a) * p.B + j);
-    } else if (!active) {
-        return;
-    }
-    const float proj = (float)sum * ra.step;
-    if (MODE == 0) {
-        p.out[(long long)item * p.out_item_stride + (long long)a * p.B + j] = proj;
-    } else {
-        int slice, gate, iter;
-        resolve_item(p.sel, item, slice, gate, iter);
-        const long long off = (((long long)slice * p.N + gate) * p.A + a) * p.B + j;
-        const GateParam gp = p.gp[gate];
-        const float yv = p.y[off];
-        const float dv = __ldg(p.d + off);
-        const float yn = (fmaf(gp.sigma, proj, yv) - gp.sigma * dv) * gp.dual_inv;
-        p.y[off] = yn;
-        float* DY = reinterpret_cast<float*>(const_cast<char*>(base) + p.off_dy);
-        const long long e = 2 * ((long long)a * p.wy + p.pb + j);
-        const float dlt = (yn - yv) * ra.step;  // pre-scaled for A^* (see K3)
-        DY[e] = dlt;
-        DY[e - 1] = dlt;
-        if (p.proj) p.proj[off] = proj;
-        if (!isfinite(yn) && p.status)
-            atomicMin(p.status + 1, ((unsigned long long)iter << 20) | (unsigned long long)gate);
-    }
-}
 
-// Pair-packed tap vectors: G = 1 -> float2 (value, forward difference); G = 2 ->
-// float4 holding the pairs of the two items of a gate pair.
-template <int G> struct TapVec;
-template <> struct TapVec<1> { using T = float2; };
-template <> struct TapVec<2> { using T = float4; };
 __device__ __forceinline__ float tv(const float2& v, int) { return v.x; }
 __device__ __forceinline__ float td(const float2& v, int) { return v.y; }
 __device__ __forceinline__ float tv(const float4& v, int h) { return h ? v.z : v.x; }
 __device__ __forceinline__ float td(const float4& v, int h) { return h ? v.w : v.y; }
 
-#ifndef FWD_MIN_BLOCKS2
-#define FWD_MIN_BLOCKS2 8
-#endif
-
-// G = 2: one warp walks the rays of two items (a gate pair) at once; every
-// per-item sum is accumulated exactly as with G = 1 (bitwise equal results).
-template <int MODE, int LPT, int G>
-__global__ void __launch_bounds__(32 * FWD_ANGLES, G == 1 ? FWD_MIN_BLOCKS : FWD_MIN_BLOCKS2)
+// K2 walks two rays per warp lane at once, one 16-byte load per sample:
+//   MIR = 0 (gate pairs): items 2p, 2p+1 at angle a (pair region);
+//   MIR = 1 (single item): angles a and A-a of one item, the second through the
+//     column-mirrored image (item region, slot 1) -- ray (A-a, j) of W is ray
+//     (a, j) of Wm[r][c] = W[r][cols-1-c] (rows-dominant: cont' = cols-1-cont;
+//     cols-dominant: the same samples in reverse column order), so one walk and
+//     one set of fractions serve both angles.
+// Every per-ray sum is accumulated as by the one-ray walk: 8 samples per trip,
+// fp32 partial sums per 64 samples, fp64 totals.
+template <int MODE, int LPT, int MIR>
+__global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_MIN_BLOCKS2)
     fwd_kernel(FwdArgs p) {
-    using V = typename TapVec<G>::T;
+    using V = float4;
+    constexpr int G = 2;
     const int ks = p.ksplit;
-    const int group = blockIdx.z / ks;  // item (G = 1) or gate pair (G = 2)
+    const int group = blockIdx.z / ks;  // item (MIR) or gate pair
     const int part = blockIdx.z - group * ks;
     // LPT (single-gate launches): grid (angle groups, bin tiles by distance rank, parts): every angle group's
     // central tiles (the longest rays) are dispatched before any edge tile, so the
@@ -397,21 +229,26 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, G == 1 ? FWD_MIN_BLOCKS : FWD
         const int r = jr - 2 * pairs;
         return below > above ? c - 1 - pairs - r : c + 1 + pairs + r;
     }() : (int)blockIdx.x;
-    const int a_raw = (LPT ? blockIdx.x : blockIdx.y) * FWD_ANGLES + threadIdx.y;
-    const bool warp_on = a_raw < p.A;        // warp-uniform; no early exit (block syncs below)
-    const int a = warp_on ? a_raw : p.A - 1;
+    const int s_raw = (LPT ? blockIdx.x : blockIdx.y) * FWD_ANGLES + threadIdx.y;
+    const int nslot = MIR ? mir_slots(p.A) : p.A;
+    const bool warp_on = s_raw < nslot;      // warp-uniform; no early exit (block syncs below)
+    const int sl = warp_on ? s_raw : nslot - 1;
+    const int nsingle = MIR ? mir_nsingle(p.A) : 0;
+    // angle walked by this warp (slot 0); MIR: slot 1 is angle A - a
+    const int a = !MIR ? sl : (sl < nsingle ? (sl == 0 ? 0 : p.A / 2) : sl - nsingle + 1);
+    const bool pair1 = !MIR || sl >= nsingle;  // slot 1 holds a real ray
     const int j = btile * 32 + threadIdx.x;
     const bool active = warp_on && j < p.B;
     const int jj = active ? j : p.B - 1;  // idle lanes shadow the last bin (no store)
     const RayAngle ra = p.ang[a];
-    const int item0 = G * group;  // pair launches start at item 0
+    const int item0 = MIR ? p.item0 + group : G * group;  // pair launches start at item 0
     const char* base0 = p.ws + mct_item_off(item0, p.item_bytes, p.pair_block);  // counters
-    const char* tb = G == 1 ? base0 : p.ws + mct_pair_off(group, p.item_bytes, p.pair_block);
+    const char* tb = MIR ? base0 : p.ws + mct_pair_off(group, p.item_bytes, p.pair_block);
     const int cd = ra.cols_dom;
     // tap index = hi(fx) >= 0: the row pad is folded into fx so the address is one
     // unsigned 32x64 multiply-add
     const V* __restrict__ X2 = reinterpret_cast<const V*>(
-        tb + (G == 1 ? (cd ? p.off_xt : p.off_x) : (cd ? p.off_pxt : p.off_px)));
+        tb + (MIR ? (cd ? p.off_xt : p.off_x) : (cd ? p.off_pxt : p.off_px)));
     const int stride = cd ? p.wxt : p.wx;
     const int nmaj = cd ? p.cols : p.rows;
     const int lim = cd ? p.rows : p.cols;
@@ -479,7 +316,7 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, G == 1 ? FWD_MIN_BLOCKS : FWD
 #pragma unroll
                 for (int q = 0; q < 4; ++q) s[h][q] = t[h][q] = 0.0f;
             int kk = kc;
-            // 8 samples per trip: all 8 loads are issued before the first use
+            // 8 samples per trip
             for (; kk + 7 <= kend; kk += 8) {
                 unsigned lo8[8], hi8[8];
                 lo8[0] = flo;
@@ -540,7 +377,9 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, G == 1 ? FWD_MIN_BLOCKS : FWD
 #pragma unroll
         for (int h = 0; h < G; ++h) tot[h] = dacc[h] + (double)ea[h];
     }
-    constexpr int nval = G;
+    // ray h of this lane: item and angle
+    auto ray_item = [&](int h) { return MIR ? item0 : item0 + h; };
+    auto ray_angle = [&](int h) { return (MIR && h) ? p.A - a : a; };
     double sum[G];
 #pragma unroll
     for (int h = 0; h < G; ++h) sum[h] = tot[h];
@@ -549,11 +388,11 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, G == 1 ? FWD_MIN_BLOCKS : FWD
         if (active) {
 #pragma unroll
             for (int h = 0; h < G; ++h) {
-                if (h < nval) {
+                if (h == 0 || pair1) {
                     double* PART = reinterpret_cast<double*>(
-                        const_cast<char*>(p.ws) + mct_item_off(item0 + h, p.item_bytes, p.pair_block) +
-                        p.off_part);
-                    PART[((long long)part * p.A + a) * p.B + j] = tot[h];
+                        const_cast<char*>(p.ws) +
+                        mct_item_off(ray_item(h), p.item_bytes, p.pair_block) + p.off_part);
+                    PART[((long long)part * p.A + ray_angle(h)) * p.B + j] = tot[h];
                 }
             }
         }
@@ -582,11 +421,12 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, G == 1 ? FWD_MIN_BLOCKS : FWD
 #endif
 #pragma unroll
         for (int h = 0; h < G; ++h) {
-            if (h < nval) {
+            if (h == 0 || pair1) {
                 const double* PART = reinterpret_cast<const double*>(
-                    p.ws + mct_item_off(item0 + h, p.item_bytes, p.pair_block) + p.off_part);
+                    p.ws + mct_item_off(ray_item(h), p.item_bytes, p.pair_block) + p.off_part);
                 double acc = 0.0;
-                for (int q = 0; q < ks; ++q) acc += __ldcg(PART + ((long long)q * p.A + a) * p.B + j);
+                for (int q = 0; q < ks; ++q)
+                    acc += __ldcg(PART + ((long long)q * p.A + ray_angle(h)) * p.B + j);
                 sum[h] = acc;
             }
         }
@@ -595,28 +435,33 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, G == 1 ? FWD_MIN_BLOCKS : FWD
     }
 #pragma unroll
     for (int h = 0; h < G; ++h) {
-        if (h >= nval) break;
-        const int item = item0 + h;
+        if (h == 1 && !pair1) break;
+        const int item = ray_item(h), ah = ray_angle(h);
         const float proj = (float)sum[h] * ra.step;
         if (MODE == 0) {
-            p.out[(long long)item * p.out_item_stride + (long long)a * p.B + j] = proj;
+            p.out[(long long)item * p.out_item_stride + (long long)ah * p.B + j] = proj;
         } else {
             int slice, gate, iter;
             resolve_item(p.sel, item, slice, gate, iter);
-            const long long off = (((long long)slice * p.N + gate) * p.A + a) * p.B + j;
+            const long long off = (((long long)slice * p.N + gate) * p.A + ah) * p.B + j;
             const GateParam gp = p.gp[gate];
             const float yv = p.y[off];
             const float dv = __ldg(p.d + off);
             const float yn = (fmaf(gp.sigma, proj, yv) - gp.sigma * dv) * gp.dual_inv;
             p.y[off] = yn;
-            // DY2 element j (pair of item `item`): own region (G = 1) or the item's
-            // half of the pair region's float4 element (G = 2)
+            // DY element (row, j), float2 slot: gate pairs (a, item & 1); mirror
+            // layout (pair row q, h) or (0, self-paired slot)
+            int row = ah, slot = h;
+            if (MIR) {
+                row = sl < nsingle ? 0 : a;
+                slot = sl < nsingle ? sl : h;
+            }
             float* DY = reinterpret_cast<float*>(const_cast<char*>(tb) +
-                                                 (G == 1 ? p.off_dy : p.off_pdy)) + 2 * h;
-            const long long e = 2 * G * ((long long)a * p.wy + p.pb + j);
+                                                 (MIR ? p.off_dy : p.off_pdy)) + 2 * slot;
+            const long long e = 4 * ((long long)row * p.wy + p.pb + j);
             const float dlt = (yn - yv) * ra.step;  // pre-scaled for A^* (see K3)
             DY[e] = dlt;
-            DY[e - 2 * G + 1] = dlt;
+            DY[e - 3] = dlt;
             if (p.proj) p.proj[off] = proj;
             if (!isfinite(yn) && p.status)
                 atomicMin(p.status + 1, ((unsigned long long)iter << 20) | (unsigned long long)gate);
@@ -664,18 +509,26 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, G == 1 ? FWD_MIN_BLOCKS : FWD
 #endif
 #define INV_2_32 2.3283064365386963e-10f
 
-// One tent (bin index thi, fraction tlo/2^32) applied to two sinogram rows: row
-// thi's (pixel p at angle a) and row thi + delta's (the mirror of p at A-a), for
-// the G items whose pair-packed rows share the float2 / float4 elements.
+// One tent (bin index thi, fraction tlo/2^32) applied to two sinogram rows, the
+// row of pixel p at angle a and the row of its mirror at A-a:
+//   G = 1 (single item, mirror DY layout): both rows share the float4 element
+//     (slot 0: angle a, slot 1: angle A-a) -- one 16-byte load;
+//   G = 2 (gate pairs): rows a and a + delta of the pair region, each float4
+//     holding the two items' pairs.
 template <int K, int G>
-__device__ __forceinline__ void adj_tap2(const typename TapVec<G>::T* __restrict__ DY2, unsigned tlo,
-                                         int thi, int delta, float g32, float omg, float* acc_a,
+__device__ __forceinline__ void adj_tap2(const float4* __restrict__ DY2, unsigned tlo, int thi,
+                                         int delta, float g32, float omg, float* acc_a,
                                          float* acc_b) {
-    using V = typename TapVec<G>::T;
     const float F = (float)tlo;
-    if (K == 0) {
-        const V v = __ldg(DY2 + (unsigned)thi);
-        const V vm = __ldg(DY2 + (unsigned)(thi + delta));
+    if (K == 0 && G == 1) {
+        const float4 v = __ldg(DY2 + (unsigned)thi);
+        const float w0 = __saturatef(fmaf(-F, g32, 1.0f));  // bin floor(jc)
+        const float w1 = __saturatef(fmaf(F, g32, omg));    // bin floor(jc) + 1
+        acc_a[0] = fmaf(w0, v.x, fmaf(w1, v.y, acc_a[0]));
+        acc_b[0] = fmaf(w0, v.z, fmaf(w1, v.w, acc_b[0]));
+    } else if (K == 0) {
+        const float4 v = __ldg(DY2 + (unsigned)thi);
+        const float4 vm = __ldg(DY2 + (unsigned)(thi + delta));
         const float w0 = __saturatef(fmaf(-F, g32, 1.0f));  // bin floor(jc)
         const float w1 = __saturatef(fmaf(F, g32, omg));    // bin floor(jc) + 1
 #pragma unroll
@@ -688,40 +541,53 @@ __device__ __forceinline__ void adj_tap2(const typename TapVec<G>::T* __restrict
         const float g = g32 * 4294967296.0f;
 #pragma unroll
         for (int mm = -K; mm <= K; mm += 2) {
-            const V v = __ldg(DY2 + (thi + mm));
-            const V vm = __ldg(DY2 + (thi + delta + mm));
             const float wa = __saturatef(fmaf(-fabsf((float)mm - d), g, 1.0f));
             const float wb = __saturatef(fmaf(-fabsf((float)(mm + 1) - d), g, 1.0f));
+            if (G == 1) {
+                const float4 v = __ldg(DY2 + (thi + mm));
+                acc_a[0] = fmaf(wa, v.x, fmaf(wb, v.y, acc_a[0]));
+                acc_b[0] = fmaf(wa, v.z, fmaf(wb, v.w, acc_b[0]));
+            } else {
+                const float4 v = __ldg(DY2 + (thi + mm));
+                const float4 vm = __ldg(DY2 + (thi + delta + mm));
 #pragma unroll
-            for (int h = 0; h < G; ++h) {
-                acc_a[h] = fmaf(wa, tv(v, h), fmaf(wb, td(v, h), acc_a[h]));
-                acc_b[h] = fmaf(wa, tv(vm, h), fmaf(wb, td(vm, h), acc_b[h]));
+                for (int h = 0; h < G; ++h) {
+                    acc_a[h] = fmaf(wa, tv(v, h), fmaf(wb, td(v, h), acc_a[h]));
+                    acc_b[h] = fmaf(wa, tv(vm, h), fmaf(wb, td(vm, h), acc_b[h]));
+                }
             }
         }
     }
 }
 
+// One tent on one sinogram row: G = 1: float2 slot `slot` of the element; G = 2:
+// both items' pairs.
 template <int K, int G>
-__device__ __forceinline__ void adj_tap1(const typename TapVec<G>::T* __restrict__ DY2, unsigned tlo,
-                                         int thi, float g32, float omg, float* acc) {
-    using V = typename TapVec<G>::T;
+__device__ __forceinline__ void adj_tap1(const float4* __restrict__ DY2, unsigned tlo, int thi,
+                                         int slot, float g32, float omg, float* acc) {
     const float F = (float)tlo;
     if (K == 0) {
-        const V v = __ldg(DY2 + (unsigned)thi);
+        const float4 v = __ldg(DY2 + (unsigned)thi);
         const float w0 = __saturatef(fmaf(-F, g32, 1.0f));
         const float w1 = __saturatef(fmaf(F, g32, omg));
+        if (G == 1)
+            acc[0] = fmaf(w0, tv(v, slot), fmaf(w1, td(v, slot), acc[0]));
+        else
 #pragma unroll
-        for (int h = 0; h < G; ++h) acc[h] = fmaf(w0, tv(v, h), fmaf(w1, td(v, h), acc[h]));
+            for (int h = 0; h < G; ++h) acc[h] = fmaf(w0, tv(v, h), fmaf(w1, td(v, h), acc[h]));
     } else {
         const float d = F * INV_2_32;
         const float g = g32 * 4294967296.0f;
 #pragma unroll
         for (int mm = -K; mm <= K; mm += 2) {
-            const V v = __ldg(DY2 + (thi + mm));
+            const float4 v = __ldg(DY2 + (thi + mm));
             const float wa = __saturatef(fmaf(-fabsf((float)mm - d), g, 1.0f));
             const float wb = __saturatef(fmaf(-fabsf((float)(mm + 1) - d), g, 1.0f));
+            if (G == 1)
+                acc[0] = fmaf(wa, tv(v, slot), fmaf(wb, td(v, slot), acc[0]));
+            else
 #pragma unroll
-            for (int h = 0; h < G; ++h) acc[h] = fmaf(wa, tv(v, h), fmaf(wb, td(v, h), acc[h]));
+                for (int h = 0; h < G; ++h) acc[h] = fmaf(wa, tv(v, h), fmaf(wb, td(v, h), acc[h]));
         }
     }
 }
@@ -747,7 +613,7 @@ template <> struct AdjShape<2> {
 // load per pixel-angle).  Per-item arithmetic identical to G = 1.
 template <int K, int G>
 __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(AdjArgs p) {
-    using V = typename TapVec<G>::T;
+    using V = float4;
     constexpr int PPT = AdjShape<G>::PPT;
     constexpr int TH = PPT * ADJ_WARPS;
     __shared__ longlong2 s_t[ADJ_CH];  // anchor (with sinogram row base of a), cos/sp
@@ -787,10 +653,11 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
         const int nsingle = (A % 2 == 0 && A >= 2) ? 2 : 1;
         for (int si = 0; si < nsingle; ++si) {
             const int a = si == 0 ? 0 : A / 2;
+            const int arow = G == 1 ? 0 : a;  // mirror layout: row 0, slot si
             const AdjAngle aa = p.ang[a];
             const double jcA = v0 * aa.cs - u0 * aa.sn + p.jmid;
             const long long TA =
-                __double2ll_rn(jcA * FX_ONE) + ((long long)(a * p.wy + p.pb) << 32);
+                __double2ll_rn(jcA * FX_ONE) + ((long long)(arow * p.wy + p.pb) << 32);
             const float g32 = aa.g * INV_2_32, omg = 1.0f - aa.g;
             long long T = TA + (long long)txc * aa.csx - row_off * aa.snx;
             long long Tm = TA + (long long)(cmc - c0) * aa.csx - row_off * aa.snx;
@@ -798,8 +665,8 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
                 float acc[G], accm[G];
 #pragma unroll
                 for (int h = 0; h < G; ++h) acc[h] = accm[h] = 0.0f;
-                adj_tap1<K, G>(DY2, (unsigned)T, (int)(T >> 32), g32, omg, acc);
-                adj_tap1<K, G>(DY2, (unsigned)Tm, (int)(Tm >> 32), g32, omg, accm);
+                adj_tap1<K, G>(DY2, (unsigned)T, (int)(T >> 32), si, g32, omg, acc);
+                adj_tap1<K, G>(DY2, (unsigned)Tm, (int)(Tm >> 32), si, g32, omg, accm);
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
                     s_tot[h][m][tid] += (double)acc[h];
@@ -914,19 +781,22 @@ cudaError_t launch_pad_sino(const float* sino, const mct_ray_plan* rp, char* ws,
     return cudaGetLastError();
 }
 
+// K2 ray split of single-item launches (a plan constant, see MCT_KSPLIT_MIN):
+// enough parts to fill about one wave of resident blocks.
 int choose_ksplit(int A, int B, int n) {
     static int slots = 0;  // resident fwd blocks per GPU (queried once)
     if (slots == 0) {
-        int dev = 0, sms = 148, per_sm = FWD_MIN_BLOCKS;
+        int dev = 0, sms = 148, per_sm = FWD_MIN_BLOCKS2;
         if (cudaGetDevice(&dev) == cudaSuccess)
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fwd_kernel1<1, 1>, 32 * FWD_ANGLES,
-                                                          0) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fwd_kernel<1, 1, 1>,
+                                                          32 * FWD_ANGLES, 0) != cudaSuccess ||
             per_sm < 1)
-            per_sm = FWD_MIN_BLOCKS;
+            per_sm = FWD_MIN_BLOCKS2;
         slots = sms * per_sm;
     }
-    const long long blocks = (long long)((B + 31) / 32) * ((A + FWD_ANGLES - 1) / FWD_ANGLES);
+    const long long blocks =
+        (long long)((B + 31) / 32) * ((mir_slots(A) + FWD_ANGLES - 1) / FWD_ANGLES);
     long long k = (slots + blocks - 1) / blocks;
     const long long by_len = n / 16 > 1 ? n / 16 : 1;  // >= 16 samples per part
     k = k < by_len ? k : by_len;
@@ -945,50 +815,51 @@ static void fwd_prefer_l1() {
 #ifdef FWD_CARVEOUT_PCT
     const int pct = FWD_CARVEOUT_PCT;
 #else
-    const int pct = 7;  // >= 12 blocks x 1 KB reserved of 228 KB -> the 16 KB config
+    const int pct = 7;  // >= 8 blocks x 1 KB reserved of 228 KB -> the 16 KB config
 #endif
-    cudaFuncSetAttribute(fwd_kernel1<0, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute(fwd_kernel1<1, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute(fwd_kernel1<0, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute(fwd_kernel1<1, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute(fwd_kernel<0, 0, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute(fwd_kernel<1, 0, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel<0, 0, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel<1, 0, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel<0, 0, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel<1, 0, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel<0, 1, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(fwd_kernel<1, 1, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
 cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st) {
     fwd_prefer_l1();
     FwdArgs a = a_in;
     dim3 block(32, FWD_ANGLES);
-    const unsigned ntile = (a.B + 31) / 32, ngroup = (a.A + FWD_ANGLES - 1) / FWD_ANGLES;
+    const unsigned ntile = (a.B + 31) / 32;
     const int np = mct_pair_items(items);
     if (np > 0) {  // gate pairs (bins fastest: L2 locality across pairs)
         a.item0 = 0;
-        dim3 grid(ntile, ngroup, (np / 2) * a.ksplit);
+        dim3 grid(ntile, (a.A + FWD_ANGLES - 1) / FWD_ANGLES, (np / 2) * a.ksplit);
         if (mode == 0)
-            fwd_kernel<0, 0, 2><<<grid, block, 0, st>>>(a);
+            fwd_kernel<0, 0, 0><<<grid, block, 0, st>>>(a);
         else
-            fwd_kernel<1, 0, 2><<<grid, block, 0, st>>>(a);
+            fwd_kernel<1, 0, 0><<<grid, block, 0, st>>>(a);
         if (np == items) return cudaGetLastError();
     }
-    // single items (an odd last item after the pairs).  One single-gate item:
-    // longest-rays-first dispatch order (LPT) shrinks the last partial wave; with
-    // many items the item-major order keeps better L2 locality.  Same arithmetic
-    // either way (block order only).
+    // single items (mirror-angle walks; an odd last item after the pairs).  One
+    // single-gate item: longest-rays-first dispatch order (LPT) shrinks the last
+    // partial wave; with several items the item-major order keeps better L2
+    // locality.  Same arithmetic either way (block order only).
     a.item0 = np;
     const int rest = items - np;
+    const unsigned ngroup = (mir_slots(a.A) + FWD_ANGLES - 1) / FWD_ANGLES;
     const bool lpt = a.ksplit > 1 && rest == 1;
     dim3 grid(lpt ? ngroup : ntile, lpt ? ntile : ngroup, rest * a.ksplit);
     if (lpt) {
         if (mode == 0)
-            fwd_kernel1<0, 1><<<grid, block, 0, st>>>(a);
+            fwd_kernel<0, 1, 1><<<grid, block, 0, st>>>(a);
         else
-            fwd_kernel1<1, 1><<<grid, block, 0, st>>>(a);
+            fwd_kernel<1, 1, 1><<<grid, block, 0, st>>>(a);
         return cudaGetLastError();
     }
     if (mode == 0)
-        fwd_kernel1<0, 0><<<grid, block, 0, st>>>(a);
+        fwd_kernel<0, 0, 1><<<grid, block, 0, st>>>(a);
     else
-        fwd_kernel1<1, 0><<<grid, block, 0, st>>>(a);
+        fwd_kernel<1, 0, 1><<<grid, block, 0, st>>>(a);
     return cudaGetLastError();
 }
 
