@@ -57,8 +57,10 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
                         const double* sin_a, const uint8_t* rows_dominant);
 int mct_ray_plan_destroy(mct_ray_plan* plan);
 
-/* Bytes of device workspace one standalone forward/adjoint call needs per batch
- * item (padded image copies + padded sinogram + image scratch).               */
+/* Bytes of device workspace a standalone forward/adjoint call of up to `batch`
+ * items needs (padded image copies + padded sinogram + image scratch per item,
+ * plus one interleaved gate-pair region per item pair: launches of >= 2 items
+ * process items 2p, 2p+1 together).  Not linear in `batch`; size with this.  */
 size_t mct_ray_workspace_bytes(const mct_ray_plan* plan, int batch);
 
 /* A: x_dev (batch, rows, cols) -> sino_dev (batch, A, B).  projector.py:201-207 */
@@ -122,7 +124,8 @@ int mct_family_destroy(mct_family* fam);
 int mct_family_set_params(mct_family* fam, const double* sigmas, const double* probs,
                           double theta);
 
-/* Workspace bytes for `items` concurrently processed (slice,gate) items.       */
+/* Workspace bytes for launches of up to `items` (slice,gate) items (pair blocks,
+ * see mct_ray_workspace_bytes).                                                */
 size_t mct_family_workspace_bytes(const mct_family* fam, int items);
 
 /* Standalone gated forward / adjoint of one (slice, gate): A(D x), D^*(A^* y). */
