@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
 #define ADJ_CH ADJ_THREADS
 #endif
 #ifndef ADJ_MIN_BLOCKS
-#define ADJ_MIN_BLOCKS 10
+#define ADJ_MIN_BLOCKS 7   // single-item A^* (72 registers; fewer, longer angle splits)
 #endif
 #ifndef ADJ_SPLIT_RULE
 #define ADJ_SPLIT_RULE 1
