@@ -301,6 +301,10 @@ def test_dense_gated_parity_full_size(m, n, peak):
     (64, 64, 200, 91, 1.0),     # the reference's default angle count (45 deg is cols-dominant)
 ])
 def test_edge_geometries_vs_oracle(m, g):
+    """Single items (mirror-angle kernels) and a batch of 3 (one gate pair + an odd
+    last item) against the fp64 oracle on every edge geometry."""
+    import torch
+
     r = np.random.default_rng(sum(int(v) for v in g[:4]))
     geom = m.Geometry(*g)
     op = m.RayTransform(geom)
@@ -309,6 +313,13 @@ def test_edge_geometries_vs_oracle(m, g):
     y = r.standard_normal(geom.sino_shape).astype(np.float32).astype(np.float64)
     assert rel_l2(op.apply(x), orc.apply(x)) <= TOL
     assert rel_l2(op.adjoint_apply(y), orc.adjoint_apply(y)) <= TOL
+    xb = r.standard_normal((3,) + tuple(geom.image_shape)).astype(np.float32)
+    yb = r.standard_normal((3,) + tuple(geom.sino_shape)).astype(np.float32)
+    fb = op.forward_batch(torch.from_numpy(xb).cuda()).double().cpu().numpy()
+    ab = op.adjoint_batch(torch.from_numpy(yb).cuda()).double().cpu().numpy()
+    for i in range(3):
+        assert rel_l2(fb[i], orc.apply(xb[i].astype(np.float64))) <= TOL, i
+        assert rel_l2(ab[i], orc.adjoint_apply(yb[i].astype(np.float64))) <= TOL, i
 
 
 def test_too_fine_detector_rejected(m):
