@@ -504,6 +504,9 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
 #ifndef ADJ_MIN_BLOCKS
 #define ADJ_MIN_BLOCKS 7   // single-item A^* (72 registers; fewer, longer angle splits)
 #endif
+#ifndef ADJ_PATCH
+#define ADJ_PATCH 0    // 1: 8 x 4 pixel patches per warp (see adj_kernel)
+#endif
 #ifndef ADJ_SPLIT_RULE
 #define ADJ_SPLIT_RULE 1
 #endif
@@ -629,11 +632,17 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
     const int tid = threadIdx.y * ADJ_TW + threadIdx.x;
     const int ncl = (p.cols + 1) >> 1;                      // left-half columns (incl. centre)
     const int r0 = blockIdx.y * TH, c0 = blockIdx.x * ADJ_TW;
-    const int c = c0 + threadIdx.x;                          // primary column
+    // lane -> pixels: ADJ_PATCH = 0: a warp is 32 columns, a thread PPT consecutive
+    // rows; ADJ_PATCH = 1: a warp is 8 columns x 4 rows, a thread rows rb, rb+4, ...
+    // (the same 32 x TH tile and per-pixel arithmetic either way)
+    constexpr int RSTEP = ADJ_PATCH ? 4 : 1;
+    const int lcol = ADJ_PATCH ? (int)threadIdx.y * 8 + ((int)threadIdx.x & 7) : (int)threadIdx.x;
+    const int rbase = ADJ_PATCH ? ((int)threadIdx.x >> 3) : (int)threadIdx.y * PPT;
+    const int c = c0 + lcol;                                 // primary column
     const int cm = p.cols - 1 - c;                           // mirror column
-    const int rt = r0 + threadIdx.y * PPT;
-    const int nrows = min(PPT, p.rows - rt);                 // warp-uniform
-    const int txc = min((int)threadIdx.x, ncl - 1 - c0);     // clamp lanes past the half
+    const int rt = r0 + rbase;
+    const int nrows = rt < p.rows ? min(PPT, (p.rows - rt + RSTEP - 1) / RSTEP) : 0;
+    const int txc = min(lcol, ncl - 1 - c0);                 // clamp lanes past the half
     const int cmc = p.cols - 1 - (c0 + txc);                 // (clamped) mirror column
     const double u0 = (double)r0 - 0.5 * (double)(p.rows - 1);
     const double v0 = (double)c0 - 0.5 * (double)(p.cols - 1);
@@ -641,7 +650,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
     const char* tb = G == 1 ? p.ws + mct_item_off(item0, p.item_bytes, p.pair_block)
                             : p.ws + mct_pair_off(item0 >> 1, p.item_bytes, p.pair_block);
     const V* __restrict__ DY2 = reinterpret_cast<const V*>(tb + (G == 1 ? p.off_dy : p.off_pdy));
-    const long long row_off = (long long)(threadIdx.y * PPT);
+    const long long row_off = (long long)rbase;
 
 #pragma unroll
     for (int h = 0; h < G; ++h)
@@ -672,8 +681,8 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
                     s_tot[h][m][tid] += (double)acc[h];
                     s_tot[h][PPT + m][tid] += (double)accm[h];
                 }
-                T -= aa.snx;
-                Tm -= aa.snx;
+                T -= RSTEP * aa.snx;
+                Tm -= RSTEP * aa.snx;
             }
         }
     }
@@ -706,6 +715,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
             const int4 U = s_u[t];
             const int delta = s_d[t];
             const long long snx = ((long long)U.y << 32) | (unsigned)U.x;
+            const long long snr = RSTEP * snx;  // per-row step of this thread's rows
             const float g32 = __int_as_float(U.z), omg = __int_as_float(U.w);
             // c at angle a == cm at angle A-a ; cm at angle a == c at angle A-a
             const long long T = T2.x + (long long)txc * T2.y - row_off * snx;
@@ -718,8 +728,8 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
                     adj_tap2<K, G>(DY2, tlo, (int)thi, delta, g32, omg, acc[m], accm[m]);
                     adj_tap2<K, G>(DY2, mlo, (int)mhi, delta, g32, omg, accm[m], acc[m]);
                 }
-                fx_sub(tlo, thi, (unsigned)U.x, (unsigned)U.y);
-                fx_sub(mlo, mhi, (unsigned)U.x, (unsigned)U.y);
+                fx_sub(tlo, thi, (unsigned)snr, (unsigned)(snr >> 32));
+                fx_sub(mlo, mhi, (unsigned)snr, (unsigned)(snr >> 32));
             }
         }
 #pragma unroll
@@ -737,7 +747,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
             const_cast<char*>(p.ws) + mct_item_off(item0 + h, p.item_bytes, p.pair_block) +
             p.off_img + (size_t)split * p.img_slot_bytes);
         for (int m = 0; m < nrows; ++m) {
-            const long long row = (long long)(rt + m) * p.cols;
+            const long long row = (long long)(rt + RSTEP * m) * p.cols;
             if (cm == c) {  // centre column of an odd width: the primary role already
                 IMG[row + c] = (float)s_tot[h][m][tid];  // holds every angle (mirror = duplicate)
             } else {
