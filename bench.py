@@ -386,7 +386,9 @@ def run_ours(args, cfg):
     ab = alg_bytes(cfg)
     iter_ms = sum(kern.values())
     dominant = max(("K2_forward_dual", "K3_adjoint"), key=lambda k: kern[k])
-    traffic = load_traffic().get(dominant) if cfg.name == "c3" else None
+    tr = load_traffic()
+    traffic = tr.get(dominant) if cfg.name == "c3" else None
+    l1_frac = (tr.get("l1_data_pipe_frac") or {}).get(dominant) if cfg.name == "c3" else None
     if traffic is not None:  # captured on the 20-item C3 launch: scale to this launch
         traffic = traffic * items_per_launch / TRAFFIC_ITEMS
     ws_mb = (eng.ws.numel() + 4 * (eng.y.numel() + eng.d.numel() + 4 * eng.x.numel())) / 1e6
@@ -495,7 +497,10 @@ def run_ours(args, cfg):
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved,
                          "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                          "traffic": traffic, "peak_source": peak_src,
-                         "bytes_model": "SpMV-equivalent algorithmic bytes, SURVEY.md §8d"},
+                         "bytes_model": "SpMV-equivalent algorithmic bytes, SURVEY.md §8d",
+                         "l1_data_pipe_frac": l1_frac,
+                         "limiter": "L1 data pipe (taps served from L1/L2; ncu LSU wavefronts "
+                                    "vs peak, profiles/ncu_traffic.json)"},
             "roofline_pair": {"achieved_alg_gbs": pair_gbs, "frac_alg": pair_gbs / hbm_peak,
                               "achieved_min_gbs": min_gbs, "frac_min": min_gbs / hbm_peak,
                               "joseph_samples_per_s": 2 * ab["S"] * items_per_launch /
@@ -682,7 +687,10 @@ def run_batch_ours(args, cfg):
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved,
                          "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                          "traffic": traffic, "peak_source": peak_src,
-                         "bytes_model": "SpMV-equivalent algorithmic bytes, SURVEY.md §8d"},
+                         "bytes_model": "SpMV-equivalent algorithmic bytes, SURVEY.md §8d",
+                         "l1_data_pipe_frac": l1_frac,
+                         "limiter": "L1 data pipe (taps served from L1/L2; ncu LSU wavefronts "
+                                    "vs peak, profiles/ncu_traffic.json)"},
             "roofline_pair": {"achieved_alg_gbs": pair_gbs, "frac_alg": pair_gbs / hbm_peak},
             "kernel_ms_per_epoch_rank0": kern,
             "e2e": e2e,

@@ -1,4 +1,5 @@
-"""Write profiles/ncu_traffic.json: DRAM bytes per launch of K2 / K3 from an ncu --set full report."""
+"""Write profiles/ncu_traffic.json from an ncu --set full report: DRAM bytes per launch of
+K1-K4 and each kernel's L1 data-pipe (LSU wavefront) utilisation, the limiter of K2/K3."""
 import csv
 import json
 import subprocess
@@ -22,6 +23,8 @@ for r in rows[2:]:
            else 'K1_prox_warp' if 'pack_kernel' in name else 'K4_adjoint_update'
            if 'update_kernel' in name else name)
     out[key] = tot
+    i = hdr.index('l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed')
+    out.setdefault('l1_data_pipe_frac', {})[key] = float(r[i].replace(',', '')) / 100.0
 out['source'] = Path(rep).name + ' (C3, 20-item PDHG launch, ncu --set full --clock-control none)'
 Path('profiles').mkdir(exist_ok=True)
 Path('profiles/ncu_traffic.json').write_text(json.dumps(out, indent=1) + '\n')
