@@ -441,3 +441,25 @@ def test_power_method_contract_on_device(m):
     n = 7
     blocks = [m.IdentityMap((5,)) for _ in range(n)]
     assert abs(m.stacked_norm_sq(blocks, iterations=50, seed=0) - n) <= 1e-6
+
+
+def test_mass_conservation_within_sampling_ripple(m):
+    """test_projector.py:107-116: integrating each angle's projection over the
+    detector recovers the image mass up to the interpolation ripple."""
+    geom = m.Geometry.fast()
+    x = m.make_phantom("nested_shells", 64, 64)
+    sino = m.forward(geom, x)
+    mass = x.sum()
+    per_angle = sino.sum(axis=1) * geom.detector_spacing
+    assert np.max(np.abs(per_angle - mass)) / mass <= 2.5e-3
+
+
+def test_terminal_warp_norms_stay_near_isometric(m):
+    """test_motion.py:108-122: the norm window the step sizes rely on, at the
+    largest motion state of each preset family (device power iteration)."""
+    rigid = m.MotionParams(kind="rigid", rotation=m.motion.RIGID_TERMINAL_ROTATION,
+                           translation=m.motion.RIGID_TERMINAL_TRANSLATION)
+    dila = m.MotionParams(kind="dilatation", scale=1.0 + m.motion.DILATATION_TERMINAL_GROWTH)
+    for params in (rigid, dila):
+        norm = m.power_method(m.WarpOperator(params, (64, 64)), iterations=150, seed=0)
+        assert 0.8 <= norm <= 1.2, params.kind

@@ -412,3 +412,23 @@ def test_fused_iterations_stay_inside_workspace(m, golden_tiny, mode):
     torch.cuda.synchronize()
     assert bool((ws[need:] == 0xAB).all()), "workspace tail overwritten"
     assert np.array_equal(eng.x[0].double().cpu().numpy(), x_ref)
+
+
+@pytest.mark.parametrize("mode,draws", [("pdhg", [(0, 1, 2, 3)]),
+                                        ("spdhg", [(1,), (0,), (2,), (3,), (2,)])])
+def test_saddle_is_fixed_point(m, golden_tiny, mode, draws):
+    """test_solvers.py:337-370: started at a saddle point (x*, y*) with
+    z = zbar = sum_i A_i^* y*_i, a full-draw step and a single-gate sequence leave
+    x in place (device CG saddle, fp32 iterates)."""
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    saddle = m.cg_reference(problem)
+    z = sum(op.adjoint_apply(y) for op, y in zip(problem.operators, saddle.y_star))
+    state = m.SolverState(x=saddle.x_star, y=list(saddle.y_star), z=z, zbar=z)
+    cfg = tiny_config(m, G, mode, 0, epochs=1)
+    for d in draws:
+        m.step(state, cfg, problem, lambda d=d: d)
+    scale = float(np.linalg.norm(saddle.x_star))
+    assert np.linalg.norm(state.x - saddle.x_star) <= 1e-4 * scale
+    for y_new, y_old in zip(state.y, saddle.y_star):
+        assert np.linalg.norm(y_new - y_old) <= 1e-4 * max(1.0, float(np.linalg.norm(y_old)))
