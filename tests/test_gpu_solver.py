@@ -432,3 +432,62 @@ def test_saddle_is_fixed_point(m, golden_tiny, mode, draws):
     assert np.linalg.norm(state.x - saddle.x_star) <= 1e-4 * scale
     for y_new, y_old in zip(state.y, saddle.y_star):
         assert np.linalg.norm(y_new - y_old) <= 1e-4 * max(1.0, float(np.linalg.norm(y_old)))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_p2p_exchange_emulated_ranks(m, golden_tiny, world):
+    """The multi-rank exchange protocol on one GPU: W virtual ranks (one engine per
+    gate shard, each with its own partial buffers and signal pad), driven through
+    the real mct_exchange_post / mct_exchange_z_update kernels.  Every rank posts
+    before any rank updates (stream order), so no kernel waits on another -- the
+    data flow (parity buffers, per-iteration flags, rank-order sum) is exercised
+    without concurrent ranks.  All ranks end with identical bits, equal to a
+    host-ordered sum of the same partials and to the single-process run."""
+    import torch
+
+    from paper_2410_10503_b200 import _lib
+    from paper_2410_10503_b200.distributed import ShardedPDHG, exchange_schedule
+
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    cfg = tiny_config(m, G, "pdhg", 0, epochs=6)
+    x_run, _ = m.run(cfg, problem, diagnostics=False)
+    L = _lib.load()
+    st = _lib.stream_handle()
+    ws = [ShardedPDHG(cfg, problem, r, world) for r in range(world)]
+    n = ws[0].engine.x.numel()
+    parts = [[torch.zeros(n, device="cuda") for _ in range(2)] for _ in range(world)]
+    pads = [torch.zeros(world, dtype=torch.int64, device="cuda") for _ in range(world)]
+    failed = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(world)]
+    pads_dev = torch.tensor([p.data_ptr() for p in pads], dtype=torch.int64, device="cuda")
+    parts_dev = [torch.tensor([parts[r][k].data_ptr() for r in range(world)], dtype=torch.int64,
+                              device="cuda") for k in (0, 1)]
+    ref = ShardedPDHG(cfg, problem, 0, world)  # host-ordered sum of the same partials
+    refs = [ShardedPDHG(cfg, problem, r, world) for r in range(1, world)]
+    for e in range(cfg.epochs):
+        flag, parity = exchange_schedule(e)
+        for r, w in enumerate(ws):
+            w.engine.iteration(w.engine.items_pdhg(epoch_ctr=True), problem.alpha,
+                               dz=parts[r][parity].view(w.engine.x.shape))
+        for r in range(world):
+            _lib.check(L.mct_exchange_post(_lib.ptr(pads_dev), world, r, flag, st))
+        for r, w in enumerate(ws):
+            _lib.check(L.mct_exchange_z_update(_lib.ptr(parts_dev[parity]), pads[r].data_ptr(),
+                                               world, flag, n, _lib.ptr(w.engine.z),
+                                               _lib.ptr(w.engine.zbar), float(cfg.theta),
+                                               _lib.ptr(failed[r]), st))
+            w.engine.advance_epoch()
+        dzs = [w.local_iteration().clone() for w in [ref] + refs]
+        total = dzs[0].clone()
+        for d in dzs[1:]:
+            total += d  # rank order, fp32
+        for w in [ref] + refs:
+            w.finish(total)
+    torch.cuda.synchronize()
+    assert all(int(f.item()) == 0 for f in failed)
+    assert all(int(v) == cfg.epochs for p in pads for v in p.cpu().numpy())
+    xs = [w.engine.x[0].double().cpu().numpy() for w in ws]
+    for x in xs[1:]:
+        assert np.array_equal(x, xs[0])
+    assert np.array_equal(xs[0], ref.engine.x[0].double().cpu().numpy())
+    assert rel_l2(xs[0], x_run) <= 1e-6
