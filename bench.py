@@ -615,6 +615,7 @@ def run_batch_ours(args, cfg):
     # kern[*] sums one epoch: num_gates launches, each over the S local slices
     achieved = ab[dominant] * S * cfg.num_gates / (kern[dominant] * 1e-3) / 1e9
     traffic = None  # the committed ncu traffic capture is of the C3 20-gate launch
+    l1_frac = None
     pair_gbs = ab["pair"] * cfg.batch * cfg.num_gates / (ms_step * 1e-3) / 1e9
 
     # e2e: every step uploads the local slices' sinograms from pinned host memory
