@@ -279,6 +279,16 @@ class SolverState:
         self._last = dict(last_projections or {})
 
     @classmethod
+    def _device_zero(cls) -> "SolverState":
+        """A zero-counter state whose arrays live on a device engine (bound by run()
+        to its engine after reset): no host copies of the N dual blocks."""
+        st = cls.__new__(cls)
+        st._engine = st._problem = st._host = None
+        st.iteration, st.epoch, st.fwd_calls, st.adj_calls = 0, 0.0, 0, 0
+        st._last = {}
+        return st
+
+    @classmethod
     def zeros(cls, problem: Problem) -> "SolverState":
         shape = problem.image_shape
         return cls(x=np.zeros(shape), y=[np.zeros(d.shape) for d in problem.data],
@@ -404,10 +414,10 @@ def run(config: SolverConfig, problem: Problem, saddle: SaddlePoint | None = Non
     """
     if config.num_gates != problem.num_gates:
         raise ValueError("config and problem disagree on the gate count")
-    state = SolverState.zeros(problem)
     record = ConvergenceRecord()
     if config.epochs == 0:
         return np.zeros(problem.image_shape), record
+    state = SolverState._device_zero()  # bound to the engine below (no host arrays)
     torch = _lib.require_cuda()
     keep = diagnostics and config.mode == "pdhg"
     eng = problem._engine(keep)  # zero state below == SolverState.zeros(problem)
