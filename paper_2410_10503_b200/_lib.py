@@ -165,12 +165,13 @@ REDUCE_PARTS = 128
 _SCRATCH = {}
 
 
-def scratch(device, segments: int = 1):
+def scratch(device, segments: int = 1, stream: int | None = None):
     """Cached fp64 scratch for the two-pass reductions (per device and stream, so
-    reductions issued on different streams never share partials)."""
+    reductions issued on different streams never share partials).  ``stream``: the
+    raw handle when the caller already has it (saves the torch stream query)."""
     import torch
 
-    key = (str(device), stream_handle())
+    key = (str(device), stream_handle() if stream is None else stream)
     need = REDUCE_PARTS * max(1, segments)
     t = _SCRATCH.get(key)
     if t is None or t.numel() < need:

@@ -297,14 +297,17 @@ class Engine:
             t.copy_(v)
 
     # ---------------------------------------------------------- diagnostics
-    def reduce(self, a, b, segments: int, length: int, mode: int, out=None):
-        """Fixed-order fp64 reduction of ``segments`` runs of ``length`` (into ``out``)."""
+    def reduce(self, a, b, segments: int, length: int, mode: int, out=None, st=None):
+        """Fixed-order fp64 reduction of ``segments`` runs of ``length`` (into ``out``).
+        ``st``: the current stream's raw handle, when the caller already holds it."""
         if out is None:
             out = self.torch.empty(segments, dtype=self.torch.float64, device=self.device)
+        if st is None:
+            st = _lib.stream_handle()
+        optr = out if isinstance(out, int) else _lib.ptr(out)  # a tensor or a raw device address
         _lib.check(_lib.load().mct_reduce(_lib.ptr(a), _lib.ptr(b) if b is not None else None,
-                                          length, segments, length, mode, _lib.ptr(out),
-                                          _lib.ptr(_lib.scratch(self.device, segments)),
-                                          _lib.stream_handle()))
+                                          length, segments, length, mode, optr,
+                                          _lib.ptr(_lib.scratch(self.device, segments, st)), st))
         return out
 
     def gated_forward(self, slice_index: int, gate: int, x, out):
@@ -318,7 +321,7 @@ class Engine:
                                                  _lib.ptr(y), _lib.ptr(out), _lib.ptr(self.ws),
                                                  _lib.stream_handle()))
 
-    def objective_parts(self, reuse_projections: bool, fit_out=None, xx_out=None):
+    def objective_parts(self, reuse_projections: bool, fit_out=None, xx_out=None, st=None):
         """Device fp64 parts of the objective, no host sync: ||A_i x - d_i||^2 per
         (slice, gate) and ||x||^2 per slice (written into ``fit_out`` / ``xx_out``)."""
         torch = self.torch
@@ -329,18 +332,18 @@ class Engine:
                 self._proj_scratch = torch.empty_like(self.y)
             proj = self._proj_scratch
             if self.max_items >= self.N:  # all gates of a slice in one pass
+                h = st if st is not None else _lib.stream_handle()
                 for s in range(self.S):
                     _lib.check(_lib.load().mct_gated_forward_many(
                         self.family.handle, s, _lib.ptr(self.all_gates), self.N,
-                        _lib.ptr(self.x[s]), _lib.ptr(proj[s]), _lib.ptr(self.ws),
-                        _lib.stream_handle()))
+                        _lib.ptr(self.x[s]), _lib.ptr(proj[s]), _lib.ptr(self.ws), h))
             else:
                 for s in range(self.S):
                     for g in range(self.N):
                         self.gated_forward(s, g, self.x[s], proj[s, g])
         fit = self.reduce(proj, self.d, self.S * self.N, self.n_sino, _lib.REDUCE_SQDIFF,
-                          out=fit_out)
-        xx = self.reduce(self.x, None, self.S, self.n_img, _lib.REDUCE_SQDIFF, out=xx_out)
+                          out=fit_out, st=st)
+        xx = self.reduce(self.x, None, self.S, self.n_img, _lib.REDUCE_SQDIFF, out=xx_out, st=st)
         return fit, xx
 
     def objectives(self, alpha: float, reuse_projections: bool):

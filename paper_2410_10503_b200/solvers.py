@@ -447,6 +447,8 @@ def run(config: SolverConfig, problem: Problem, saddle: SaddlePoint | None = Non
     table = torch.full((config.epochs, cols), math.nan, dtype=torch.float64, device=eng.device)
     sync_every = 1 if on_epoch is not None else SYNC_EPOCHS
     pending = []
+    st = _lib.stream_handle()  # one stream per run: query it once
+    table_ptr = _lib.ptr(table)
 
     def flush():
         if not pending:
@@ -483,15 +485,16 @@ def run(config: SolverConfig, problem: Problem, saddle: SaddlePoint | None = Non
         state.adj_calls += n
         if config.mode == "pdhg":
             state.last_projections = {i: None for i in range(n)}
-        row = table[epoch_index - 1]
+        fit_row = table_ptr + 8 * cols * (epoch_index - 1)  # raw fp64 addresses of the row
+        xx_row, xd_row, yd_row, tr_row = (fit_row + 8 * (n + k) for k in range(4))
         if diagnostics:
-            eng.objective_parts(config.mode == "pdhg", fit_out=row[:n], xx_out=row[n:n + 1])
+            eng.objective_parts(config.mode == "pdhg", fit_out=fit_row, xx_out=xx_row, st=st)
         if xs is not None:
-            eng.reduce(eng.x[0], xs, 1, eng.n_img, _lib.REDUCE_SQDIFF, out=row[n + 1:n + 2])
-            eng.reduce(eng.y[0], ys, 1, eng.N * eng.n_sino, _lib.REDUCE_SQDIFF,
-                       out=row[n + 2:n + 3])
+            eng.reduce(eng.x[0], xs, 1, eng.n_img, _lib.REDUCE_SQDIFF, out=xd_row, st=st)
+            eng.reduce(eng.y[0], ys, 1, eng.N * eng.n_sino, _lib.REDUCE_SQDIFF, out=yd_row,
+                       st=st)
         if tr is not None:
-            eng.reduce(eng.x[0], tr, 1, eng.n_img, _lib.REDUCE_SQDIFF, out=row[n + 3:n + 4])
+            eng.reduce(eng.x[0], tr, 1, eng.n_img, _lib.REDUCE_SQDIFF, out=tr_row, st=st)
         pending.append(epoch_index)
         if len(pending) >= sync_every or epoch_index == config.epochs:
             flush()
