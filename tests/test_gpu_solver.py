@@ -491,3 +491,21 @@ def test_p2p_exchange_emulated_ranks(m, golden_tiny, world):
         assert np.array_equal(x, xs[0])
     assert np.array_equal(xs[0], ref.engine.x[0].double().cpu().numpy())
     assert rel_l2(xs[0], x_run) <= 1e-6
+
+
+def test_run_batch_pdhg_odd_gates_equals_single_runs(m):
+    """Multi-slice PDHG launches with an odd gate count: gate pairs straddle the
+    slice boundary (slice 0 gate 2 with slice 1 gate 0) and the last item runs
+    alone; every slice still matches its own run()."""
+    from paper_2410_10503_b200 import workloads
+
+    cfgw = workloads.WorkloadConfig("batch_pdhg", 48, 40, 71, 3, "dense", 5, 1e-2, 3, peak=3.0)
+    probs = [m.simulate.workload_problem(cfgw, s)[0] for s in range(2)]
+    norms = [m.power_method(op, iterations=20) for op in probs[0].operators]
+    stacked = float(sum(v * v for v in norms))
+    cfgs = [m.default_config("pdhg", norms, cfgw.alpha, cfgw.epochs, seed=0,
+                             stacked_norm_sq=stacked) for _ in range(2)]
+    out = m.run_batch(cfgs, probs)
+    for (xb, _), c, p in zip(out, cfgs, probs):
+        xs, _ = m.run(c, p, diagnostics=False)
+        assert rel_l2(xb, xs) <= 1e-6
