@@ -347,7 +347,10 @@ def run_ours(args, cfg):
             worker.reduce_update(dz_now[0])
         eng.advance_epoch()
 
-    launches_per_step = (7 if exchange == "p2p" else 6) if use_dist else 5
+    # K2 / K3 run one launch for the gate pairs and one for an odd last item
+    n_items = eng.local * eng.S
+    per_kernel = int(n_items >= 2) + (n_items % 2)
+    launches_per_step = 3 + 2 * per_kernel + ((2 if exchange == "p2p" else 1) if use_dist else 0)
     for _ in range(args.warmup):
         step_fn()
     if use_dist and exchange == "p2p" and worker.p2p_failed_anywhere():
@@ -696,7 +699,8 @@ def run_batch_ours(args, cfg):
             "kernel_ms_per_epoch_rank0": kern,
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": (4 * cfg.num_gates + 1) * args.steps,
+            # per iteration: K1, K4 and K2 / K3 for the slice pairs (+ an odd last slice)
+            "gpu_launches": ((2 + 2 * (int(S >= 2) + S % 2)) * cfg.num_gates + 1) * args.steps,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
