@@ -255,9 +255,9 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     off += align256((size_t)(num_angles / 2 + 1) * p->wy * sizeof(float4));
     p->off_img = off;
     p->img_slot_bytes = align256((size_t)rows * cols * sizeof(float));
-    // A^* partial-image slots: the largest angle split any launch of this plan
-    // uses is the single-item one (choose_asplit is non-increasing in items)
-    off += p->img_slot_bytes * (size_t)choose_asplit(p, 1);
+    // A^* partial-image slots: the largest angle split any launch of this plan may
+    // use (choose_asplit never exceeds it)
+    off += p->img_slot_bytes * (size_t)adj_plan_slots(p);
     p->off_part = off;
     p->ksplit1 = choose_ksplit(num_angles, num_bins, std::max(rows, cols));
     off += align256((size_t)p->ksplit1 * num_angles * num_bins * sizeof(double));

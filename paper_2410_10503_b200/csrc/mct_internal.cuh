@@ -250,6 +250,7 @@ cudaError_t launch_pad_sino(const float* sino, const mct_ray_plan* rp, char* ws,
 cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st);
 cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, cudaStream_t st);
 int choose_asplit(const mct_ray_plan* rp, int items);
+int adj_plan_slots(const mct_ray_plan* rp);
 int choose_ksplit(int A, int B, int n);
 cudaError_t launch_update(const UpdArgs& a, int mode, int slices, cudaStream_t st);
 cudaError_t launch_z_update(long long n, const float* dz, float* z, float* zbar, float theta,

@@ -923,6 +923,22 @@ static long long adj_slots(int G) {
     return slots[G];
 }
 
+// A^* partial-image slots a plan's items hold: the single-item split, and at
+// least MCT_MIN_ASLOTS so multi-gate launches with an odd last item (gate-sharded
+// ranks) can split too.
+#ifndef MCT_MIN_ASLOTS
+#define MCT_MIN_ASLOTS 4
+#endif
+int adj_plan_slots(const mct_ray_plan* rp) {
+    constexpr int TH1 = AdjShape<1>::PPT * ADJ_WARPS;
+    const long long tiles1 = (long long)adj_tiles_x(rp->cols) * ((rp->rows + TH1 - 1) / TH1);
+    const int s1 = adj_split_for(tiles1, adj_slots(1), rp);
+    const long long by_angles =
+        rp->A / (2 * MCT_ASPLIT_MIN_PAIRS) > 0 ? rp->A / (2 * MCT_ASPLIT_MIN_PAIRS) : 1;
+    const int lo = (int)(by_angles < MCT_MIN_ASLOTS ? by_angles : MCT_MIN_ASLOTS);
+    return s1 > lo ? s1 : lo;
+}
+
 int choose_asplit(const mct_ray_plan* rp, int items) {
     const int n = items > 0 ? items : 1;
     constexpr int TH1 = AdjShape<1>::PPT * ADJ_WARPS, TH2 = AdjShape<2>::PPT * ADJ_WARPS;
@@ -942,7 +958,8 @@ int choose_asplit(const mct_ray_plan* rp, int items) {
     const long long by_angles =
         rp->A / (2 * MCT_ASPLIT_MIN_PAIRS) > 0 ? rp->A / (2 * MCT_ASPLIT_MIN_PAIRS) : 1;
     long long smax = by_angles < MCT_MAX_ASPLIT ? by_angles : MCT_MAX_ASPLIT;
-    smax = smax < s1 ? smax : s1;
+    const long long cap = adj_plan_slots(rp);
+    smax = smax < cap ? smax : cap;
     long long best = 1, best_cost = -1;
     for (long long sp = 1; sp <= smax; ++sp) {
         const long long waves = (b2 * sp + sl2 - 1) / sl2 + (b1 * sp + sl1 - 1) / sl1;
