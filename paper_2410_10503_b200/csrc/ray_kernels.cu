@@ -8,6 +8,10 @@
 
 #include <math.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 namespace {
 
 // Angle slots of a single-item (mirror) launch: slot s < nsingle is a
@@ -835,41 +839,96 @@ static void fwd_prefer_l1() {
     cudaFuncSetAttribute(fwd_kernel<1, 1, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
+// A launch with gate pairs and an odd last item runs the two (independent) grids
+// concurrently: the odd item's on a side stream forked from and joined back to
+// the caller's stream with events (graph-capture safe).  One side stream per
+// (device, caller stream), so concurrent callers on different streams never share
+// one; events are per call.
+#ifndef MCT_SIDE_STREAM
+#define MCT_SIDE_STREAM 1
+#endif
+static cudaStream_t side_stream_for(cudaStream_t st) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, cudaStream_t> streams;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_pair(dev, st);
+    auto it = streams.find(key);
+    if (it != streams.end()) return it->second;
+    cudaStream_t side = nullptr;
+    if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    streams[key] = side;
+    return side;
+}
+
+template <class MainF, class SideF>
+static cudaError_t fork_join(cudaStream_t st, MainF main_launch, SideF side_launch) {
+    cudaStream_t side = MCT_SIDE_STREAM ? side_stream_for(st) : nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    if (side == nullptr || cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess) {
+        if (fork) cudaEventDestroy(fork);
+        main_launch(st);  // serial fallback on the caller's stream
+        side_launch(st);
+        return cudaGetLastError();
+    }
+    cudaError_t e = cudaEventRecord(fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
+    if (e == cudaSuccess) {
+        side_launch(side);
+        main_launch(st);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(join, side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, join, 0);
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+    return e;
+}
+
 cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st) {
     fwd_prefer_l1();
-    FwdArgs a = a_in;
-    dim3 block(32, FWD_ANGLES);
-    const unsigned ntile = (a.B + 31) / 32;
+    const dim3 block(32, FWD_ANGLES);
+    const unsigned ntile = (a_in.B + 31) / 32;
     const int np = mct_pair_items(items);
-    if (np > 0) {  // gate pairs (bins fastest: L2 locality across pairs)
+    // gate pairs (bins fastest: L2 locality across pairs)
+    auto pairs = [&](cudaStream_t s) {
+        FwdArgs a = a_in;
         a.item0 = 0;
         dim3 grid(ntile, (a.A + FWD_ANGLES - 1) / FWD_ANGLES, (np / 2) * a.ksplit);
         if (mode == 0)
-            fwd_kernel<0, 0, 0><<<grid, block, 0, st>>>(a);
+            fwd_kernel<0, 0, 0><<<grid, block, 0, s>>>(a);
         else
-            fwd_kernel<1, 0, 0><<<grid, block, 0, st>>>(a);
-        if (np == items) return cudaGetLastError();
-    }
+            fwd_kernel<1, 0, 0><<<grid, block, 0, s>>>(a);
+    };
     // single items (mirror-angle walks; an odd last item after the pairs).  One
     // single-gate item: longest-rays-first dispatch order (LPT) shrinks the last
     // partial wave; with several items the item-major order keeps better L2
     // locality.  Same arithmetic either way (block order only).
-    a.item0 = np;
-    const int rest = items - np;
-    const unsigned ngroup = (mir_slots(a.A) + FWD_ANGLES - 1) / FWD_ANGLES;
-    const bool lpt = a.ksplit > 1 && rest == 1;
-    dim3 grid(lpt ? ngroup : ntile, lpt ? ntile : ngroup, rest * a.ksplit);
-    if (lpt) {
-        if (mode == 0)
-            fwd_kernel<0, 1, 1><<<grid, block, 0, st>>>(a);
-        else
-            fwd_kernel<1, 1, 1><<<grid, block, 0, st>>>(a);
-        return cudaGetLastError();
-    }
-    if (mode == 0)
-        fwd_kernel<0, 0, 1><<<grid, block, 0, st>>>(a);
+    auto singles = [&](cudaStream_t s) {
+        FwdArgs a = a_in;
+        a.item0 = np;
+        const int rest = items - np;
+        const unsigned ngroup = (mir_slots(a.A) + FWD_ANGLES - 1) / FWD_ANGLES;
+        const bool lpt = a.ksplit > 1 && rest == 1;
+        dim3 grid(lpt ? ngroup : ntile, lpt ? ntile : ngroup, rest * a.ksplit);
+        if (lpt) {
+            if (mode == 0)
+                fwd_kernel<0, 1, 1><<<grid, block, 0, s>>>(a);
+            else
+                fwd_kernel<1, 1, 1><<<grid, block, 0, s>>>(a);
+        } else if (mode == 0) {
+            fwd_kernel<0, 0, 1><<<grid, block, 0, s>>>(a);
+        } else {
+            fwd_kernel<1, 0, 1><<<grid, block, 0, s>>>(a);
+        }
+    };
+    if (np > 0 && items > np) return fork_join(st, pairs, singles);
+    if (np > 0)
+        pairs(st);
     else
-        fwd_kernel<1, 0, 1><<<grid, block, 0, st>>>(a);
+        singles(st);
     return cudaGetLastError();
 }
 
@@ -989,15 +1048,21 @@ static void launch_adj_g(const AdjArgs& a, int kfoot, int groups, cudaStream_t s
 // angle split (K4 sums the same number of partial slots for every item).
 cudaError_t launch_adj(const AdjArgs& a_in, int kfoot, int items, cudaStream_t st) {
     if (kfoot < 0 || kfoot > 3) return cudaErrorInvalidValue;
-    AdjArgs a = a_in;
     const int np = mct_pair_items(items);
-    if (np > 0) {
+    auto pairs = [&](cudaStream_t s) {
+        AdjArgs a = a_in;
         a.item0 = 0;
-        launch_adj_g<2>(a, kfoot, np / 2, st);
-    }
-    if (items > np) {
+        launch_adj_g<2>(a, kfoot, np / 2, s);
+    };
+    auto singles = [&](cudaStream_t s) {
+        AdjArgs a = a_in;
         a.item0 = np;
-        launch_adj_g<1>(a, kfoot, items - np, st);
-    }
+        launch_adj_g<1>(a, kfoot, items - np, s);
+    };
+    if (np > 0 && items > np) return fork_join(st, pairs, singles);  // concurrent
+    if (np > 0)
+        pairs(st);
+    else
+        singles(st);
     return cudaGetLastError();
 }
