@@ -158,8 +158,8 @@ __global__ void pad_sino_kernel(const float* __restrict__ sino, const AdjAngle* 
 
 // ---------------------------------------------------------------------------
 // K2: Joseph forward A (projector.py:201-207 with the weights of :160-183).
-// Block = 16 warps = 16 consecutive angles x 32 consecutive bins: the warps walk
-// nearly the same image lines, so most taps hit L1.
+// Block = FWD_ANGLES (4) warps = 4 consecutive angle slots x 32 consecutive bins:
+// the warps walk nearly the same image lines, so most taps hit L1.
 // Along the dominant axis the continuous minor index advances by a constant
 // slope.  It is carried in 32.32 fixed point whose integer part also carries
 // the row offset, so one 64-bit add advances both, the integer part is the
@@ -187,10 +187,6 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
 #define FWD_ACQREL 1
 #endif
 #define FWD_ANGLES MCT_FWD_ANGLES  // warps (= consecutive angles) per block; they share L1 lines
-#ifndef FWD_MIN_BLOCKS
-#define FWD_MIN_BLOCKS 12         // 12 x 4 warps resident: 40 registers for 8 loads in flight
-#endif
-
 #ifndef FWD_MIN_BLOCKS2
 #define FWD_MIN_BLOCKS2 8         // gate pairs: 8 x 4 warps resident, 64 registers
 #endif
@@ -198,8 +194,7 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
 #define FWD_MIN_BLOCKS_M 7        // single-item mirror walks (72 registers, no spills)
 #endif
 
-__device__ __forceinline__ float tv(const float2& v, int) { return v.x; }
-__device__ __forceinline__ float td(const float2& v, int) { return v.y; }
+// (value, forward difference) of float2 slot h of a float4 element
 __device__ __forceinline__ float tv(const float4& v, int h) { return h ? v.z : v.x; }
 __device__ __forceinline__ float td(const float4& v, int h) { return h ? v.w : v.y; }
 
