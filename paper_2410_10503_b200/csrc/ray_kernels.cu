@@ -851,6 +851,11 @@ static cudaStream_t side_stream_for(cudaStream_t st) {
     auto key = std::make_pair(dev, st);
     auto it = streams.find(key);
     if (it != streams.end()) return it->second;
+    // never create a stream while the caller's stream is being captured (a global-mode
+    // capture would be invalidated): such a first call runs serially instead
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+        return nullptr;
     cudaStream_t side = nullptr;
     if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
     streams[key] = side;

@@ -509,3 +509,22 @@ def test_run_batch_pdhg_odd_gates_equals_single_runs(m):
     for (xb, _), c, p in zip(out, cfgs, probs):
         xs, _ = m.run(c, p, diagnostics=False)
         assert rel_l2(xb, xs) <= 1e-6
+
+
+def test_odd_item_fork_join_in_graph_on_user_stream(m, golden_tiny):
+    """3-item launches (a gate pair + the odd item on the library's side stream, forked
+    and joined with events) issued from a user stream and captured in the epoch CUDA
+    graph give the same iterate as eager launches on the default stream."""
+    import torch
+
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    ops = list(problem.operators)[:3]
+    sub = m.Problem.from_parts(problem.alpha, ops, list(problem.data)[:3])
+    cfg = m.default_config("pdhg", [1.0] * 3, sub.alpha, 3, stacked_norm_sq=3.0)
+    x_eager, _ = m.run(cfg, sub, graph=False, diagnostics=False)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        x_graph, _ = m.run(cfg, sub, graph=True, diagnostics=False)
+    torch.cuda.synchronize()
+    assert np.array_equal(x_eager, x_graph)
