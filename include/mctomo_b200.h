@@ -153,7 +153,11 @@ int mct_gated_forward_many(const mct_family* fam, int slice, const int32_t* gate
  * gate, items_per_slice = local gate count.  SPDHG: gates_dev = the pre-drawn
  * per-slice sequence (numpy default_rng(seed).choice, solvers.py:312),
  * slice_stride = total iterations, epoch_stride = N, base = iteration in epoch,
- * items_per_slice = 1, epoch_ctr_dev = device epoch counter (graph replay).    */
+ * items_per_slice = 1, epoch_ctr_dev = device epoch counter (graph replay).
+ * K1-K4 of one iteration must see the same mct_items (item count): launches of
+ * >= 2 items process items 2p, 2p+1 together (gate pairs) in an interleaved
+ * workspace region, an odd last item on its own (concurrently, on a library
+ * side stream joined back to `stream`); a single item pairs its mirror angles.  */
 typedef struct {
     const int32_t* gates_dev;
     const int32_t* epoch_ctr_dev; /* may be NULL */
