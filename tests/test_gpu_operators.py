@@ -463,3 +463,21 @@ def test_terminal_warp_norms_stay_near_isometric(m):
     for params in (rigid, dila):
         norm = m.power_method(m.WarpOperator(params, (64, 64)), iterations=150, seed=0)
         assert 0.8 <= norm <= 1.2, params.kind
+
+
+@pytest.mark.parametrize("batch", [3, 5])
+def test_large_batches_match_single_items(m, batch):
+    """C3-size batches with an odd item (gate pairs + the odd item on the side stream,
+    the A^* angle split chosen over both launches, up to the plan's >= 4 slots) agree
+    with single-item calls (A^* split differs, so fp32 rounding, not bits)."""
+    import torch
+
+    geom = m.Geometry(512, 512, 720, 729, 1.0)
+    op = m.RayTransform(geom)
+    x = torch.randn(batch, 512, 512, device="cuda")
+    y = torch.randn(batch, 720, 729, device="cuda")
+    fb, ab = op.forward_batch(x), op.adjoint_batch(y)
+    for i in range(batch):
+        assert rel_l2(fb[i].double().cpu().numpy(), op.apply(x[i]).double().cpu().numpy()) <= 1e-6
+        assert rel_l2(ab[i].double().cpu().numpy(),
+                      op.adjoint_apply(y[i]).double().cpu().numpy()) <= 1e-6
