@@ -528,3 +528,39 @@ def test_odd_item_fork_join_in_graph_on_user_stream(m, golden_tiny):
         x_graph, _ = m.run(cfg, sub, graph=True, diagnostics=False)
     torch.cuda.synchronize()
     assert np.array_equal(x_eager, x_graph)
+
+
+@pytest.mark.parametrize("shape,angles,bins", [((40, 56), 61, 75), ((57, 33), 90, 71)])
+def test_non_square_dense_trajectories_vs_oracle(m, shape, angles, bins):
+    """Non-square images (mirror columns of unequal halves, odd angle counts with one
+    self-paired angle), 3 dense gates (a gate pair + the odd item) and a rigid gate:
+    PDHG and SPDHG trajectories vs the fp64 oracle."""
+    rng = np.random.default_rng(7)
+    rows, cols = shape
+    geom = m.Geometry(rows, cols, angles, bins, 1.0)
+    yy, xx = np.mgrid[0:rows, 0:cols].astype(np.float64)
+    specs = []
+    for g in range(3):
+        cy, cx = rng.uniform(0, rows), rng.uniform(0, cols)
+        bump = np.exp(-((yy - cy) ** 2 + (xx - cx) ** 2) / (2 * 12.0 ** 2))
+        amp = rng.uniform(-2.5, 2.5, 2)
+        specs.append(np.stack([amp[0] * bump, amp[1] * bump]).astype(np.float32))
+    specs.append(m.MotionParams(kind="rigid", rotation=0.05, translation=(1.5, -0.7)))
+    ops = m.gate_operators(geom, specs)
+    truth = rng.uniform(0, 1, shape).astype(np.float32).astype(np.float64)
+    data = [np.asarray(op.apply(truth)) + 0.01 * rng.standard_normal(geom.sino_shape)
+            for op in ops]
+    data = [d.astype(np.float32).astype(np.float64) for d in data]
+    problem = m.Problem.from_parts(1e-2, ops, data)
+    norms = [m.power_method(op, iterations=30) for op in ops]
+    ospecs = [{"kind": "dense", "phi": sp} for sp in specs[:3]] + [
+        {"kind": "rigid", "rotation": 0.05, "translation": (1.5, -0.7)}]
+    oops = oracle.gate_operators(oracle.Geometry(rows, cols, angles, bins, 1.0), ospecs,
+                                 threads=oracle.default_threads())
+    for mode in ("pdhg", "spdhg"):
+        cfg = m.default_config(mode, norms, 1e-2, 3, seed=4)
+        x, rec = m.run(cfg, problem)
+        ocfg = osolver.default_config(mode, norms, 1e-2, 3, seed=4)
+        st, objs = osolver.run(ocfg, 1e-2, oops, data)
+        assert rel_l2(x, st.x) <= ITER_TOL, mode
+        assert np.allclose(rec.objective, objs, rtol=ITER_TOL), mode
