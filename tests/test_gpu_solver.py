@@ -530,14 +530,16 @@ def test_odd_item_fork_join_in_graph_on_user_stream(m, golden_tiny):
     assert np.array_equal(x_eager, x_graph)
 
 
-@pytest.mark.parametrize("shape,angles,bins", [((40, 56), 61, 75), ((57, 33), 90, 71)])
-def test_non_square_dense_trajectories_vs_oracle(m, shape, angles, bins):
+@pytest.mark.parametrize("shape,angles,bins,sp", [((40, 56), 61, 75, 1.0), ((57, 33), 90, 71, 1.0),
+                                                  ((48, 48), 64, 101, 0.7)])
+def test_non_square_dense_trajectories_vs_oracle(m, shape, angles, bins, sp):
     """Non-square images (mirror columns of unequal halves, odd angle counts with one
-    self-paired angle), 3 dense gates (a gate pair + the odd item) and a rigid gate:
-    PDHG and SPDHG trajectories vs the fp64 oracle."""
+    self-paired angle) and a sub-pixel detector spacing (wider A^* footprint, K = 1),
+    3 dense gates and a rigid gate (gate pairs, and single items for SPDHG): PDHG and
+    SPDHG trajectories vs the fp64 oracle."""
     rng = np.random.default_rng(7)
     rows, cols = shape
-    geom = m.Geometry(rows, cols, angles, bins, 1.0)
+    geom = m.Geometry(rows, cols, angles, bins, sp)
     yy, xx = np.mgrid[0:rows, 0:cols].astype(np.float64)
     specs = []
     for g in range(3):
@@ -555,7 +557,7 @@ def test_non_square_dense_trajectories_vs_oracle(m, shape, angles, bins):
     norms = [m.power_method(op, iterations=30) for op in ops]
     ospecs = [{"kind": "dense", "phi": sp} for sp in specs[:3]] + [
         {"kind": "rigid", "rotation": 0.05, "translation": (1.5, -0.7)}]
-    oops = oracle.gate_operators(oracle.Geometry(rows, cols, angles, bins, 1.0), ospecs,
+    oops = oracle.gate_operators(oracle.Geometry(rows, cols, angles, bins, sp), ospecs,
                                  threads=oracle.default_threads())
     for mode in ("pdhg", "spdhg"):
         cfg = m.default_config(mode, norms, 1e-2, 3, seed=4)
