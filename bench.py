@@ -423,7 +423,7 @@ def run_ours(args, cfg):
         # and reads x back.  The H2D of step k+1 runs on a copy stream into the
         # second of two device data buffers while step k computes on the first.
         # (gate-sharded: each rank uploads only its own gates' sinograms)
-        glo, ghi = (worker.lo, worker.hi) if use_dist else (0, cfg.num_gates)
+        glo, ghi = (worker.data_lo, worker.data_hi) if use_dist else (0, cfg.num_gates)
         host_d = torch.from_numpy(np.stack([np.asarray(d, dtype=np.float32)
                                             for d in problem.data[glo:ghi]])[None]).pin_memory()
         host_x = torch.empty(eng.x.shape, dtype=torch.float32).pin_memory()

@@ -171,6 +171,10 @@ typedef struct {
                                 the epoch and the absolute number is
                                 *epoch_ctr*iters_per_epoch + iteration            */
     int32_t iters_per_epoch;
+    int32_t last_part;       /* 0: every item covers all angles; 1 / 2: the last item
+                                covers only the first / second half of the angle pairs
+                                (half-gate units of gate-sharded PDHG, solvers.py has no
+                                counterpart: the partial images sum across ranks)   */
 } mct_items;
 
 /* Solver state buffers (device, fp32), slice-major.

@@ -36,6 +36,7 @@ class Items(ctypes.Structure):
         ("num_slices", c_int32),
         ("iteration", c_int32),
         ("iters_per_epoch", c_int32),
+        ("last_part", c_int32),
     ]
 
 

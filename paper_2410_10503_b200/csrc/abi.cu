@@ -51,6 +51,7 @@ ItemSel make_sel(const mct_items* it) {
     s.num_slices = it->num_slices;
     s.iteration = it->iteration;
     s.iters_per_epoch = it->iters_per_epoch;
+    s.last_part = it->last_part;
     return s;
 }
 
@@ -68,6 +69,9 @@ int check_items(const mct_family* fam, const mct_items* it) {
     MCT_REQUIRE(it->items_per_slice >= 1, "items_per_slice must be >= 1");
     MCT_REQUIRE(it->num_slices >= 1 && it->num_slices <= fam->S,
                 "items.num_slices must lie in [1, family slices]");
+    MCT_REQUIRE(it->last_part >= 0 && it->last_part <= 2, "items.last_part must be 0, 1 or 2");
+    MCT_REQUIRE(it->last_part == 0 || it->num_slices == 1,
+                "a half last item needs a single-slice launch");
     return MCT_OK;
 }
 
@@ -118,6 +122,8 @@ AdjArgs adj_args(const mct_ray_plan* rp, const void* ws) {
     a.pair_block = rp->pair_block;
     a.off_pdy = rp->off_pdy;
     a.item0 = 0;
+    a.n_items = 1;
+    a.last_part = 0;
     a.asplit = 1;
     return a;
 }
@@ -689,7 +695,8 @@ int mct_iter_adjoint(const mct_family* fam, const mct_items* it, void* ws, void*
     MCT_REQUIRE(ws, "null workspace");
     AdjArgs aa = adj_args(fam->ray, ws);
     const int items = it->items_per_slice * it->num_slices;
-    aa.asplit = choose_asplit(fam->ray, items);
+    aa.last_part = it->last_part;
+    aa.asplit = choose_asplit(fam->ray, items, it->last_part);
     MCT_CUDA(launch_adj(aa, fam->ray->kfoot, items, (cudaStream_t)stream), "adjoint");
     return MCT_OK;
 }
@@ -701,7 +708,7 @@ int mct_iter_adjoint_update(const mct_family* fam, const mct_items* it, mct_stat
     MCT_REQUIRE(fam->params_set, "mct_family_set_params has not been called");
     MCT_REQUIRE(s && s->x && s->x_next && ws, "null state buffer");
     UpdArgs ua = upd_args(fam->ray, ws);
-    ua.asplit = choose_asplit(fam->ray, it->items_per_slice * it->num_slices);
+    ua.asplit = choose_asplit(fam->ray, it->items_per_slice * it->num_slices, it->last_part);
     ua.sel = make_sel(it);
     ua.N = fam->N;
     ua.warps = fam->d_warps;

@@ -102,6 +102,13 @@ struct mct_ray_plan {
 __host__ __device__ __forceinline__ int mct_pair_items(int items) {
     return MCT_PAIRS ? (items & ~1) : 0;
 }
+// ... a last item that covers only half of the angles is never paired
+__host__ __device__ __forceinline__ int mct_pair_items(int items, int last_part) {
+    return mct_pair_items(last_part ? items - 1 : items);
+}
+// Angle-pair range of a half item: part 1 = self-paired angles + pairs q in
+// [1, 1 + P/2), part 2 = pairs q in [1 + P/2, P + 1), P = (A-1)/2.
+__host__ __device__ __forceinline__ int mct_half_q(int A) { return 1 + ((A - 1) / 2) / 2; }
 
 // Byte offset of item `item`'s region and of pair p's region in a workspace.
 __host__ __device__ __forceinline__ size_t mct_item_off(int item, size_t item_bytes,
@@ -160,6 +167,7 @@ struct ItemSel {
     const int* gates;
     const int* epoch_ctr;
     int slice_stride, epoch_stride, base, ips, num_slices, iteration, iters_per_epoch;
+    int last_part;  // 0, or 1 / 2: the launch's last item covers the first / second half
 };
 
 __device__ __forceinline__ void resolve_item(const ItemSel& s, int item, int& slice, int& gate,
@@ -199,6 +207,7 @@ struct FwdArgs {
     size_t item_bytes, off_x, off_xt, off_dy, off_part, off_cnt;
     size_t pair_block, off_px, off_pxt, off_pdy;
     int item0;               // first item of the launch
+    int n_items;             // items of the whole call (the last may be a half item)
     int ksplit;
     int wy, pb;
     ItemSel sel;
@@ -222,6 +231,7 @@ struct AdjArgs {
     size_t item_bytes, off_dy, off_img, img_slot_bytes;
     size_t pair_block, off_pdy;
     int item0;               // first item of the launch
+    int n_items, last_part;  // items of the whole call; see ItemSel::last_part
     int asplit;
 };
 
@@ -248,8 +258,8 @@ cudaError_t launch_pack(const PackArgs& a, int items, cudaStream_t st);
 cudaError_t launch_pad_sino(const float* sino, const mct_ray_plan* rp, char* ws, int items,
                             cudaStream_t st);
 cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st);
-cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, cudaStream_t st);
-int choose_asplit(const mct_ray_plan* rp, int items);
+cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, cudaStream_t st);  // a.last_part
+int choose_asplit(const mct_ray_plan* rp, int items, int last_part = 0);
 int adj_plan_slots(const mct_ray_plan* rp);
 int choose_ksplit(int A, int B, int n);
 cudaError_t launch_update(const UpdArgs& a, int mode, int slices, cudaStream_t st);

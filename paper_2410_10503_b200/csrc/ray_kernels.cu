@@ -230,7 +230,12 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
     }() : (int)blockIdx.x;
     const int s_raw = (LPT ? blockIdx.x : blockIdx.y) * FWD_ANGLES + threadIdx.y;
     const int nslot = MIR ? mir_slots(p.A) : p.A;
-    const bool warp_on = s_raw < nslot;      // warp-uniform; no early exit (block syncs below)
+    bool warp_on = s_raw < nslot;            // warp-uniform; no early exit (block syncs below)
+    if (MIR && p.sel.last_part && p.item0 + (int)blockIdx.z / ks == p.n_items - 1) {
+        // a half item: slots of the first (part 1) or second (part 2) half of the angle pairs
+        const int s_mid = mir_nsingle(p.A) + mct_half_q(p.A) - 1;
+        warp_on = warp_on && (p.sel.last_part == 1 ? s_raw < s_mid : s_raw >= s_mid);
+    }
     const int sl = warp_on ? s_raw : nslot - 1;
     const int nsingle = MIR ? mir_nsingle(p.A) : 0;
     // angle walked by this warp (slot 0); MIR: slot 1 is angle A - a
@@ -626,8 +631,14 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
     const int split = blockIdx.z - group * p.asplit;
     const int A = p.A;
     const int npairs = (A - 1) / 2;  // pairs (a, A-a), a = 1 .. npairs
-    const int q_beg = 1 + (int)((long long)npairs * split / p.asplit);
-    const int q_end = 1 + (int)((long long)npairs * (split + 1) / p.asplit);
+    // angle pairs [q_lo, q_hi) of this item (a half item: one half), split evenly
+    int q_lo = 1, q_hi = npairs + 1;
+    bool singles = true;
+    const int part = (G == 1 && p.last_part && p.item0 + group == p.n_items - 1) ? p.last_part : 0;
+    if (part == 1) q_hi = mct_half_q(A);
+    if (part == 2) { q_lo = mct_half_q(A); singles = false; }
+    const int q_beg = q_lo + (int)((long long)(q_hi - q_lo) * split / p.asplit);
+    const int q_end = q_lo + (int)((long long)(q_hi - q_lo) * (split + 1) / p.asplit);
     const int tid = threadIdx.y * ADJ_TW + threadIdx.x;
     const int ncl = (p.cols + 1) >> 1;                      // left-half columns (incl. centre)
     const int r0 = blockIdx.y * TH, c0 = blockIdx.x * ADJ_TW;
@@ -657,7 +668,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
         for (int m = 0; m < 2 * PPT; ++m) s_tot[h][m][tid] = 0.0;
 
     // ---- self-paired angles 0 and A/2 (split 0 only), pixel by pixel
-    if (split == 0) {
+    if (split == 0 && singles) {
         const int nsingle = (A % 2 == 0 && A >= 2) ? 2 : 1;
         for (int si = 0; si < nsingle; ++si) {
             const int a = si == 0 ? 0 : A / 2;
@@ -770,7 +781,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
 #endif
 cudaError_t launch_pack(const PackArgs& a_in, int items, cudaStream_t st) {
     PackArgs a = a_in;
-    a.pair_items = mct_pair_items(items);
+    a.pair_items = mct_pair_items(items, a.sel.last_part);
     if (items <= PACK_SMALL_ITEMS) {  // few gates: small tiles, one halo element per thread
         dim3 grid((a.cols + 15) / 16, (a.rows + 15) / 16, items);
         pack_kernel<16, 320, PACK16_MINB><<<grid, 320, 0, st>>>(a);
@@ -891,11 +902,12 @@ cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st
     fwd_prefer_l1();
     const dim3 block(32, FWD_ANGLES);
     const unsigned ntile = (a_in.B + 31) / 32;
-    const int np = mct_pair_items(items);
+    const int np = mct_pair_items(items, a_in.sel.last_part);
     // gate pairs (bins fastest: L2 locality across pairs)
     auto pairs = [&](cudaStream_t s) {
         FwdArgs a = a_in;
         a.item0 = 0;
+        a.n_items = items;
         dim3 grid(ntile, (a.A + FWD_ANGLES - 1) / FWD_ANGLES, (np / 2) * a.ksplit);
         if (mode == 0)
             fwd_kernel<0, 0, 0><<<grid, block, 0, s>>>(a);
@@ -909,6 +921,7 @@ cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st
     auto singles = [&](cudaStream_t s) {
         FwdArgs a = a_in;
         a.item0 = np;
+        a.n_items = items;
         const int rest = items - np;
         const unsigned ngroup = (mir_slots(a.A) + FWD_ANGLES - 1) / FWD_ANGLES;
         const bool lpt = a.ksplit > 1 && rest == 1;
@@ -998,12 +1011,12 @@ int adj_plan_slots(const mct_ray_plan* rp) {
     return s1 > lo ? s1 : lo;
 }
 
-int choose_asplit(const mct_ray_plan* rp, int items) {
+int choose_asplit(const mct_ray_plan* rp, int items, int last_part) {
     const int n = items > 0 ? items : 1;
     constexpr int TH1 = AdjShape<1>::PPT * ADJ_WARPS, TH2 = AdjShape<2>::PPT * ADJ_WARPS;
     const long long tiles1 = (long long)adj_tiles_x(rp->cols) * ((rp->rows + TH1 - 1) / TH1);
     const int s1 = adj_split_for(tiles1, adj_slots(1), rp);  // single item: the plan's slot count
-    const int np = mct_pair_items(n);
+    const int np = mct_pair_items(n, last_part);
     if (np == 0) return n == 1 ? s1 : adj_split_for(tiles1 * n, adj_slots(1), rp);
     // pair launch + (odd last item) single launch run one after the other: the split
     // minimising the sum of their (waves, rounded up) x (angle pairs per block),
@@ -1048,15 +1061,17 @@ static void launch_adj_g(const AdjArgs& a, int kfoot, int groups, cudaStream_t s
 // angle split (K4 sums the same number of partial slots for every item).
 cudaError_t launch_adj(const AdjArgs& a_in, int kfoot, int items, cudaStream_t st) {
     if (kfoot < 0 || kfoot > 3) return cudaErrorInvalidValue;
-    const int np = mct_pair_items(items);
+    const int np = mct_pair_items(items, a_in.last_part);
     auto pairs = [&](cudaStream_t s) {
         AdjArgs a = a_in;
         a.item0 = 0;
+        a.n_items = items;
         launch_adj_g<2>(a, kfoot, np / 2, s);
     };
     auto singles = [&](cudaStream_t s) {
         AdjArgs a = a_in;
         a.item0 = np;
+        a.n_items = items;
         launch_adj_g<1>(a, kfoot, items - np, s);
     };
     if (np > 0 && items > np) return fork_join(st, pairs, singles);  // concurrent

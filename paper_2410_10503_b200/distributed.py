@@ -21,7 +21,7 @@ from typing import Protocol
 
 import numpy as np
 
-__all__ = ["gate_shard", "slice_shard", "sharded_epochs", "ShardedPDHG", "run_pdhg_sharded",
+__all__ = ["gate_shard", "unit_shard", "slice_shard", "sharded_epochs", "ShardedPDHG", "run_pdhg_sharded",
            "P2PExchange", "exchange_schedule"]
 
 
@@ -36,6 +36,30 @@ def _block(count: int, world: int, rank: int) -> tuple[int, int]:
 def gate_shard(num_gates: int, world: int, rank: int) -> tuple[int, int]:
     """Contiguous, balanced gate block [lo, hi) of ``rank`` (20/8 -> 3,3,3,3,2,2,2,2)."""
     return _block(num_gates, world, rank)
+
+
+def unit_shard(num_gates: int, world: int, rank: int):
+    """Half-gate units of ``rank`` (gate-sharded PDHG balanced to half a gate).
+
+    The 2N units (gate g, half h) are split into contiguous balanced blocks; a rank
+    gets the full gates [lo, hi) whose both halves it owns, plus at most one half
+    gate ``(g, part)`` at either end (part 1 = first half of the angle pairs, 2 =
+    second).  Returns ``(lo, hi, half)`` with ``half`` None when the block is
+    gate-aligned (e.g. 20 gates on 1, 2 or 4 ranks; 40 on 8)."""
+    ulo, uhi = _block(2 * num_gates, world, rank)
+    if uhi <= ulo:
+        raise ValueError("more ranks than half-gate units")
+    lo, hi = (ulo + 1) // 2, uhi // 2
+    half = None
+    if ulo % 2 == 1:
+        half = (ulo // 2, 2)
+    if uhi % 2 == 1:
+        if half is not None:  # cannot happen with balanced blocks (see DESIGN §6)
+            raise ValueError("a rank would own two half gates")
+        half = (uhi // 2, 1)
+    if half is not None and hi <= lo and uhi - ulo > 1:
+        raise ValueError("inconsistent unit block")
+    return lo, max(lo, hi), half
 
 
 def slice_shard(num_slices: int, world: int, rank: int) -> tuple[int, int]:
@@ -153,11 +177,17 @@ class ShardedPDHG:
             raise ValueError("gate sharding applies to pdhg (spdhg runs as replicas)")
         if config.num_gates != problem.num_gates:
             raise ValueError("config and problem disagree on the gate count")
-        self.lo, self.hi = gate_shard(problem.num_gates, world, rank)
-        if self.hi <= self.lo:
-            raise ValueError("more ranks than gates")
+        # half-gate units: every rank gets 2N/world units (whole gates + at most one
+        # half gate), so 20 gates on 8 ranks is 2.5 gates each instead of 3 or 2
+        self.lo, self.hi, self.half = unit_shard(problem.num_gates, world, rank)
+        if self.hi <= self.lo and self.half is None:
+            raise ValueError("more ranks than half-gate units")
+        # gates whose data this rank reads (contiguous: the half gate is lo-1 or hi)
+        hg = [self.half[0]] if self.half is not None else []
+        self.data_lo = min([self.lo] + hg)
+        self.data_hi = max([self.hi] + [g + 1 for g in hg])
         self.engine = Engine([problem.operators], [problem.data], gate_range=(self.lo, self.hi),
-                             keep_projections=keep_projections)
+                             keep_projections=keep_projections, half=self.half)
         self.engine.set_params(config)
         self.engine.reset()
         self.alpha = problem.alpha

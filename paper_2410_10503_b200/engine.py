@@ -91,7 +91,8 @@ class Engine:
 
     def __init__(self, operators_per_slice: Sequence[Sequence[LinearMap]],
                  data_per_slice: Sequence[Sequence[np.ndarray]], *, keep_projections=False,
-                 gate_range: tuple[int, int] | None = None, max_items: int | None = None):
+                 gate_range: tuple[int, int] | None = None, max_items: int | None = None,
+                 half: tuple[int, int] | None = None):
         torch = _lib.require_cuda()
         self.torch = torch
         rays, warps = [], []
@@ -118,7 +119,17 @@ class Engine:
         self.device = dev
         f32 = torch.float32
         self.gate_lo, self.gate_hi = gate_range if gate_range is not None else (0, self.N)
-        self.local = self.gate_hi - self.gate_lo
+        # half: (gate, part) -- one extra item covering the first (part 1) or second
+        # (part 2) half of that gate's angle pairs (half-gate units of gate-sharded PDHG)
+        self.half = None if half is None else (int(half[0]), int(half[1]))
+        if self.half is not None:
+            if self.half[1] not in (1, 2) or not 0 <= self.half[0] < self.N:
+                raise ValueError("half must be (gate, 1 | 2)")
+            if self.gate_lo <= self.half[0] < self.gate_hi:
+                raise ValueError("the half gate may not also be a full local gate")
+            if self.S != 1:
+                raise ValueError("half-gate units need a single slice")
+        self.local = self.gate_hi - self.gate_lo + (1 if self.half is not None else 0)
         # state
         self.x = torch.zeros((self.S, rows, cols), dtype=f32, device=dev)
         self.x_next = torch.zeros_like(self.x)
@@ -138,6 +149,9 @@ class Engine:
         self.ws = torch.zeros(int(_lib.load().mct_family_workspace_bytes(self.family.handle, items)),
                               dtype=torch.uint8, device=dev)
         self.all_gates = torch.arange(self.N, dtype=torch.int32, device=dev)
+        self.local_gates = (None if self.half is None else torch.tensor(
+            list(range(self.gate_lo, self.gate_hi)) + [self.half[0]], dtype=torch.int32,
+            device=dev))
         self.epoch_ctr = torch.zeros(1, dtype=torch.int32, device=dev)
         self.seq = None
         self._st = _lib.State()
@@ -170,12 +184,13 @@ class Engine:
     # ---------------------------------------------------------------- items
     def items_pdhg(self, iteration: int = 1, epoch_ctr: bool = False) -> _lib.Items:
         it = _lib.Items()
-        it.gates_dev = _lib.ptr(self.all_gates)
+        it.gates_dev = _lib.ptr(self.all_gates if self.half is None else self.local_gates)
         it.epoch_ctr_dev = _lib.ptr(self.epoch_ctr) if epoch_ctr else None
         it.slice_stride = 0
         it.epoch_stride = 0
-        it.base = self.gate_lo
+        it.base = self.gate_lo if self.half is None else 0
         it.items_per_slice = self.local
+        it.last_part = 0 if self.half is None else self.half[1]
         it.num_slices = self.S
         it.iteration = iteration
         it.iters_per_epoch = 1

@@ -19,7 +19,7 @@ import torch.multiprocessing as mp
 import oracle
 from oracle import solver as osolver
 from paper_2410_10503_b200 import workloads
-from paper_2410_10503_b200.distributed import gate_shard, sharded_epochs, slice_shard
+from paper_2410_10503_b200.distributed import gate_shard, sharded_epochs, slice_shard, unit_shard
 
 
 def test_gate_shard_blocks():
@@ -30,6 +30,30 @@ def test_gate_shard_blocks():
     assert [slice_shard(64, 8, r) for r in (0, 7)] == [(0, 8), (56, 64)]
     with pytest.raises(ValueError):
         gate_shard(4, 2, 2)
+
+
+@pytest.mark.parametrize("gates", [1, 2, 3, 4, 5, 7, 10, 20, 40])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_unit_shard_covers_every_half_gate_once(gates, world):
+    """Half-gate units: every (gate, half) is owned by exactly one rank, ranks hold
+    2N/world units (+-1), at most one half gate each, adjacent to their full gates."""
+    if 2 * gates < world:
+        with pytest.raises(ValueError):
+            [unit_shard(gates, world, r) for r in range(world)]
+        return
+    seen = []
+    for r in range(world):
+        lo, hi, half = unit_shard(gates, world, r)
+        units = [(g, h) for g in range(lo, hi) for h in (1, 2)]
+        if half is not None:
+            g, part = half
+            assert part in (1, 2) and (g == lo - 1 or g == hi)
+            units.append(half)
+        assert abs(len(units) - 2 * gates / world) < 1
+        seen += units
+    assert sorted(seen) == [(g, h) for g in range(gates) for h in (1, 2)]
+    assert unit_shard(20, 8, 0) == (0, 2, (2, 1)) and unit_shard(20, 8, 1) == (3, 5, (2, 2))
+    assert all(unit_shard(40, 8, r)[2] is None for r in range(8))
 
 
 class OracleShardWorker:

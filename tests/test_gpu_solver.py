@@ -434,15 +434,17 @@ def test_saddle_is_fixed_point(m, golden_tiny, mode, draws):
         assert np.linalg.norm(y_new - y_old) <= 1e-4 * max(1.0, float(np.linalg.norm(y_old)))
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 5, 8])
 def test_p2p_exchange_emulated_ranks(m, golden_tiny, world):
     """The multi-rank exchange protocol on one GPU: W virtual ranks (one engine per
     gate shard, each with its own partial buffers and signal pad), driven through
     the real mct_exchange_post / mct_exchange_z_update kernels.  Every rank posts
     before any rank updates (stream order), so no kernel waits on another -- the
     data flow (parity buffers, per-iteration flags, rank-order sum) is exercised
-    without concurrent ranks.  All ranks end with identical bits, equal to a
-    host-ordered sum of the same partials and to the single-process run."""
+    without concurrent ranks.  4 gates on 3, 5 or 8 ranks exercise the half-gate
+    units (a rank's last item covers half of the angle pairs).  All ranks end with
+    identical bits, equal to a host-ordered sum of the same partials and to the
+    single-process run."""
     import torch
 
     from paper_2410_10503_b200 import _lib

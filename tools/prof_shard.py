@@ -1,6 +1,7 @@
 """Per-kernel times of one gate-sharded PDHG iteration for local gate counts
-k = 2, 3, 5, 10, 20 (what one rank of an N-GPU run executes at C3), eager
-launches with CUDA events between the kernels (K4 in partial mode)."""
+k = 2, 2.5, 3, 5, 10, 20 (what one rank of an N-GPU run executes at C3; k.5 = k
+whole gates + one half-gate unit), eager launches with CUDA events between the
+kernels (K4 in partial mode)."""
 import argparse
 import ctypes
 import json
@@ -18,7 +19,7 @@ from paper_2410_10503_b200.engine import Engine  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
-ap.add_argument("--locals", default="2,3,5,10,20")
+ap.add_argument("--locals", default="2,2.5,3,5,10,20")
 ap.add_argument("--iters", type=int, default=20)
 args = ap.parse_args()
 cfg = workloads.CONFIGS[args.config]
@@ -34,8 +35,10 @@ c = m.default_config("pdhg", [norm] * cfg.num_gates, cfg.alpha, 1,
 L = _lib.load()
 stream = torch.cuda.current_stream()
 out = {}
-for k in [int(v) for v in args.locals.split(",")]:
-    eng = Engine([problem.operators], [problem.data], gate_range=(0, k))
+for kk in args.locals.split(","):
+    k = int(float(kk))
+    half = (k, 1) if float(kk) != k else None
+    eng = Engine([problem.operators], [problem.data], gate_range=(0, k), half=half)
     eng.set_params(c)
     eng.reset()
     dz = torch.zeros_like(eng.x)
@@ -60,8 +63,8 @@ for k in [int(v) for v in args.locals.split(",")]:
     torch.cuda.synchronize()
     t = np.array([[e[i].elapsed_time(e[i + 1]) for i in range(4)] for e in per])
     med = np.median(t, 0)
-    out[k] = {"K1": round(float(med[0]) * 1e3, 1), "K2": round(float(med[1]) * 1e3, 1),
+    out[kk] = {"K1": round(float(med[0]) * 1e3, 1), "K2": round(float(med[1]) * 1e3, 1),
               "K3": round(float(med[2]) * 1e3, 1), "K4": round(float(med[3]) * 1e3, 1),
               "sum_us": round(float(med.sum()) * 1e3, 1)}
-    print(k, json.dumps(out[k]))
+    print(kk, json.dumps(out[kk]))
     del eng
