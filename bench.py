@@ -349,7 +349,8 @@ def run_ours(args, cfg):
 
     # K2 / K3 run one launch for the gate pairs and one for an odd last item
     n_items = eng.local * eng.S
-    per_kernel = int(n_items >= 2) + (n_items % 2)
+    n_pairs = (n_items - (1 if eng.half is not None else 0)) // 2 * 2  # a half item is unpaired
+    per_kernel = int(n_pairs > 0) + int(n_items > n_pairs)
     launches_per_step = 3 + 2 * per_kernel + ((2 if exchange == "p2p" else 1) if use_dist else 0)
     for _ in range(args.warmup):
         step_fn()
