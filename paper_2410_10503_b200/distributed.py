@@ -21,7 +21,7 @@ from typing import Protocol
 
 import numpy as np
 
-__all__ = ["gate_shard", "unit_shard", "slice_shard", "sharded_epochs", "ShardedPDHG", "run_pdhg_sharded",
+__all__ = ["gate_shard", "unit_shard", "half_angle_rows", "slice_shard", "sharded_epochs", "ShardedPDHG", "run_pdhg_sharded",
            "P2PExchange", "exchange_schedule"]
 
 
@@ -60,6 +60,22 @@ def unit_shard(num_gates: int, world: int, rank: int):
     if half is not None and hi <= lo and uhi - ulo > 1:
         raise ValueError("inconsistent unit block")
     return lo, max(lo, hi), half
+
+
+def half_angle_rows(num_angles: int, part: int) -> list[int]:
+    """Sinogram rows (angles) of half ``part`` (1 or 2) of a gate: the mirror pairs
+    (q, A-q) with q < 1 + P//2 plus the self-paired angles 0 (and A/2) for part 1,
+    the remaining pairs for part 2 (P = (A-1)//2; csrc mct_half_q)."""
+    if part not in (1, 2):
+        raise ValueError("part must be 1 or 2")
+    A = int(num_angles)
+    npairs = (A - 1) // 2
+    hq = 1 + npairs // 2
+    if part == 1:
+        qs, singles = range(1, hq), [0] + ([A // 2] if A % 2 == 0 and A >= 2 else [])
+    else:
+        qs, singles = range(hq, npairs + 1), []
+    return sorted(singles + list(qs) + [A - q for q in qs])
 
 
 def slice_shard(num_slices: int, world: int, rank: int) -> tuple[int, int]:

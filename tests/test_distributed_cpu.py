@@ -1,7 +1,7 @@
-"""CPU tier: the multi-GPU host logic with gloo, world_size 2.
+"""CPU tier: the multi-GPU host logic with gloo, world_size 2 and 3.
 
 The gate-sharded PDHG protocol of paper_2410_10503_b200.distributed (contiguous
-gate blocks, replicated prox step, one allreduce(sum) of the image-sized update
+blocks of half-gate units, replicated prox step, one allreduce(sum) of the image-sized update
 per iteration, then z += dz; zbar = z + theta*dz) is driven here by an
 oracle-backed worker (test infrastructure) and must reproduce the
 single-process PDHG trajectory of the reference restatement.
@@ -19,7 +19,8 @@ import torch.multiprocessing as mp
 import oracle
 from oracle import solver as osolver
 from paper_2410_10503_b200 import workloads
-from paper_2410_10503_b200.distributed import gate_shard, sharded_epochs, slice_shard, unit_shard
+from paper_2410_10503_b200.distributed import (gate_shard, half_angle_rows, sharded_epochs,
+                                               slice_shard, unit_shard)
 
 
 def test_gate_shard_blocks():
@@ -56,26 +57,42 @@ def test_unit_shard_covers_every_half_gate_once(gates, world):
     assert all(unit_shard(40, 8, r)[2] is None for r in range(8))
 
 
+@pytest.mark.parametrize("A", [1, 2, 3, 36, 37, 720])
+def test_half_angle_rows_partition(A):
+    a, b = half_angle_rows(A, 1), half_angle_rows(A, 2)
+    assert sorted(a + b) == list(range(A))
+    assert not set(a) & set(b)
+
+
 class OracleShardWorker:
-    """Same protocol as distributed.ShardedPDHG, computed by the fp64 oracle."""
+    """Same protocol as distributed.ShardedPDHG (half-gate units: whole gates plus at
+    most one gate restricted to half of its angles), computed by the fp64 oracle."""
 
     def __init__(self, cfg, alpha, ops, data, rank, world):
         self.cfg, self.alpha, self.ops, self.data = cfg, alpha, ops, data
-        self.lo, self.hi = gate_shard(len(ops), world, rank)
+        self.lo, self.hi, half = unit_shard(len(ops), world, rank)
+        # (gate, sinogram-row mask or None)
+        self.units = [(i, None) for i in range(self.lo, self.hi)]
+        if half is not None:
+            mask = np.zeros(data[half[0]].shape[0], dtype=bool)
+            mask[half_angle_rows(len(mask), half[1])] = True
+            self.units.append((half[0], mask))
         shape = ops[0].domain_shape
         self.x = np.zeros(shape)
         self.z = np.zeros(shape)
         self.zbar = np.zeros(shape)
-        self.y = {i: np.zeros(data[i].shape) for i in range(self.lo, self.hi)}
+        self.y = {i: np.zeros(data[i].shape) for i, _ in self.units}
 
     def local_iteration(self):
         c = self.cfg
         n = len(self.ops)
         self.x_new = osolver.prox_g(self.alpha, c.tau, self.x - c.tau * self.zbar)
         dz = np.zeros_like(self.x)
-        for i in range(self.lo, self.hi):
+        for i, mask in self.units:
             proj = self.ops[i].apply(self.x_new)
             y_new = osolver.prox_fstar(n, self.data[i], c.sigmas[i], self.y[i] + c.sigmas[i] * proj)
+            if mask is not None:  # this rank owns only these angles of gate i
+                y_new = np.where(mask[:, None], y_new, self.y[i])
             dz += self.ops[i].adjoint_apply(y_new - self.y[i])
             self.y[i] = y_new
         return torch.from_numpy(dz)
@@ -154,13 +171,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("kind", ["nccl", "p2p"])
-def test_gate_sharded_pdhg_gloo_world2_matches_single_process(tmp_path, kind):
+@pytest.mark.parametrize("kind,world", [("nccl", 2), ("p2p", 2), ("nccl", 3)])
+def test_gate_sharded_pdhg_gloo_matches_single_process(tmp_path, kind, world):
+    """5 gates on 2 ranks (2.5 each: gate 2 split by angle halves) or 3 ranks."""
     out = str(tmp_path / "x.npy")
-    mp.spawn(_worker, args=(2, _free_port(), out, kind), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out, kind), nprocs=world, join=True)
     x0 = np.load(out)
-    x1 = np.load(out.replace(".npy", "_r1.npy"))
-    assert np.array_equal(x0, x1)  # replicated primal stays identical on every rank
+    for r in range(1, world):
+        # replicated primal stays identical on every rank
+        assert np.array_equal(x0, np.load(out.replace(".npy", f"_r{r}.npy")))
     cfg, alpha, ops, data = _problem()
     st, _ = osolver.run(cfg, alpha, ops, data, diagnostics=False)
     assert np.linalg.norm(x0 - st.x) <= 1e-12 * np.linalg.norm(st.x)
