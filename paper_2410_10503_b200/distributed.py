@@ -57,9 +57,7 @@ def unit_shard(num_gates: int, world: int, rank: int):
         if half is not None:  # cannot happen with balanced blocks
             raise ValueError("a rank would own two half gates")
         half = (uhi // 2, 1)
-    if half is not None and hi <= lo and uhi - ulo > 1:
-        raise ValueError("inconsistent unit block")
-    return lo, max(lo, hi), half
+    return lo, hi, half
 
 
 def half_angle_rows(num_angles: int, part: int) -> list[int]:
