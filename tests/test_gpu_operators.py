@@ -465,17 +465,19 @@ def test_terminal_warp_norms_stay_near_isometric(m):
         assert 0.8 <= norm <= 1.2, params.kind
 
 
-@pytest.mark.parametrize("batch", [3, 5])
-def test_large_batches_match_single_items(m, batch):
+@pytest.mark.parametrize("n,A,B,batch", [(512, 720, 729, 3), (512, 720, 729, 5),
+                                         (1024, 1440, 1453, 2)])
+def test_large_batches_match_single_items(m, n, A, B, batch):
     """C3-size batches with an odd item (gate pairs + the odd item on the side stream,
-    the A^* angle split chosen over both launches, up to the plan's >= 4 slots) agree
-    with single-item calls (A^* split differs, so fp32 rounding, not bits)."""
+    the A^* angle split chosen over both launches, up to the plan's >= 4 slots) and a
+    C4-size gate pair agree with single-item calls (fp32 rounding, not bits: the
+    single item walks mirror angles and may split A^* differently)."""
     import torch
 
-    geom = m.Geometry(512, 512, 720, 729, 1.0)
+    geom = m.Geometry(n, n, A, B, 1.0)
     op = m.RayTransform(geom)
-    x = torch.randn(batch, 512, 512, device="cuda")
-    y = torch.randn(batch, 720, 729, device="cuda")
+    x = torch.randn(batch, n, n, device="cuda")
+    y = torch.randn(batch, A, B, device="cuda")
     fb, ab = op.forward_batch(x), op.adjoint_batch(y)
     for i in range(batch):
         assert rel_l2(fb[i].double().cpu().numpy(), op.apply(x[i]).double().cpu().numpy()) <= 1e-6
