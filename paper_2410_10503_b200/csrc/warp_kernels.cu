@@ -13,6 +13,9 @@ namespace {
 #ifndef K4_LANES
 #define K4_LANES 4
 #endif
+#ifndef K4_MINB1
+#define K4_MINB1 0  // single-lane (single-gate) launches: compiler default
+#endif
 #ifndef K4_MINB
 #define K4_MINB 6  // register cap 42: more resident warps for the CSR gathers (C3 PDHG K4 94 -> 86 us)
 #endif
@@ -26,7 +29,7 @@ namespace {
 // sums in lane order (fixed association: deterministic), so the per-pixel gate
 // chains run LANES-wide in parallel instead of one after the other.
 template <int MODE, int LANES>
-__global__ void __launch_bounds__(256, LANES > 1 ? K4_MINB : 0) update_kernel(UpdArgs p) {
+__global__ void __launch_bounds__(256, LANES > 1 ? K4_MINB : K4_MINB1) update_kernel(UpdArgs p) {
     const int slice = blockIdx.y;
     const long long n = (long long)p.rows * p.cols;
     const int lane = LANES > 1 ? (int)threadIdx.y : 0;
