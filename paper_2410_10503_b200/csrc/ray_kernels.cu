@@ -779,6 +779,9 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
 #ifndef PACK32_MINB
 #define PACK32_MINB 6
 #endif
+#ifndef PACK32_THREADS
+#define PACK32_THREADS 256
+#endif
 cudaError_t launch_pack(const PackArgs& a_in, int items, cudaStream_t st) {
     PackArgs a = a_in;
     a.pair_items = mct_pair_items(items, a.sel.last_part);
@@ -787,7 +790,7 @@ cudaError_t launch_pack(const PackArgs& a_in, int items, cudaStream_t st) {
         pack_kernel<16, 320, PACK16_MINB><<<grid, 320, 0, st>>>(a);
     } else {
         dim3 grid((a.cols + 31) / 32, (a.rows + 31) / 32, items);
-        pack_kernel<32, 256, PACK32_MINB><<<grid, 256, 0, st>>>(a);
+        pack_kernel<32, PACK32_THREADS, PACK32_MINB><<<grid, PACK32_THREADS, 0, st>>>(a);
     }
     return cudaGetLastError();
 }
