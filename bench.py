@@ -7,12 +7,13 @@
 A "step" is one epoch (one PDHG iteration over all gates) of the C3 workload:
 512x512 fp32 random-ellipse phantom, 20 dense non-rigid gates, 720 angles x 729
 unit-spaced bins, alpha = 5e-3.  ``value`` is PDHG epochs/s (gate-sharded over
-the N ranks when N > 1: strong scaling of one problem); SPDHG epochs/s (a
-replica per rank; SPDHG does not shard) is reported beside it.
+the N ranks when N > 1 -- each rank owns 2N/ranks half-gate units -- strong
+scaling of one problem); SPDHG epochs/s (a replica per rank; SPDHG does not
+shard) is reported beside it.
 
 Timing: W warm-up epochs, then exactly K epochs bracketed by a barrier and a
 device synchronize, CUDA events on the launching stream, max over ranks.  The
-per-epoch working set (data + duals + workspace ~ 200 MB) exceeds the 126 MB L2,
+per-epoch working set (data + duals + workspace ~ 0.8 GB) exceeds the 126 MB L2,
 so no explicit flush is needed (stated in ``config``).  ``e2e`` repeats the
 measurement through the C-ABI with the step's inputs (the 20 gated sinograms)
 copied host->device from pinned memory and the result x copied back every step.
