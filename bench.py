@@ -7,7 +7,7 @@
 A "step" is one epoch (one PDHG iteration over all gates) of the C3 workload:
 512x512 fp32 random-ellipse phantom, 20 dense non-rigid gates, 720 angles x 729
 unit-spaced bins, alpha = 5e-3.  ``value`` is PDHG epochs/s (gate-sharded over
-the N ranks when N > 1 -- each rank owns 2N/ranks half-gate units -- strong
+the N ranks when N > 1 -- each rank owns 2*gates/N half-gate units -- strong
 scaling of one problem); SPDHG epochs/s (a replica per rank; SPDHG does not
 shard) is reported beside it.
 
