@@ -8,8 +8,10 @@ A "step" is one epoch (one PDHG iteration over all gates) of the C3 workload:
 512x512 fp32 random-ellipse phantom, 20 dense non-rigid gates, 720 angles x 729
 unit-spaced bins, alpha = 5e-3.  ``value`` is PDHG epochs/s (gate-sharded over
 the N ranks when N > 1 -- each rank owns 2*gates/N half-gate units -- strong
-scaling of one problem); SPDHG epochs/s (a replica per rank; SPDHG does not
-shard) is reported beside it.
+scaling of one problem); SPDHG epochs/s (an independent replica on every rank --
+SPDHG of one problem does not shard -- aggregated over the ranks) is reported
+beside it.  ``--gpus N`` with N > 1 starts the N ranks itself (torch.distributed.run,
+one rank per visible GPU) unless it already runs under a launcher.
 
 Timing: W warm-up epochs, then exactly K epochs bracketed by a barrier and a
 device synchronize, CUDA events on the launching stream, max over ranks.  The
@@ -210,7 +212,7 @@ def run_reference(args, cfg):
     threads = os.cpu_count() or 1
     port = CpuPort(cfg, threads)
     steps = max(1, min(args.steps, 400))
-    for _ in range(max(1, min(args.warmup, 2))):
+    for _ in range(args.warmup):
         port.gate_step()
     t0 = time.perf_counter()
     for _ in range(steps):
@@ -222,7 +224,7 @@ def run_reference(args, cfg):
               f"epochs of {cfg.batch} slice(s)) of the fp64 C oracle port on {threads} host threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "epochs/s",
-        "n_gpus": args.gpus, "steps": steps, "warmup": max(1, min(args.warmup, 2)),
+        "n_gpus": max(args.gpus, world), "steps": steps, "warmup": args.warmup,
         "ms_per_step": t / steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE C3 shapes)",
         "config": {"workload": f"{cfg.name}: {cfg.batch}x {cfg.n}^2, N={cfg.num_gates} "
@@ -402,21 +404,24 @@ def run_ours(args, cfg):
     min_gbs = ab["min_pair"] * items_per_launch / (iter_ms * 1e-3) / 1e9
 
     # ---------------- SPDHG (replica per rank) -----------------------------
-    spdhg = None
-    if world == 1:
-        seng = Engine([problem.operators], [problem.data])
-        seng.set_params(scfg)
-        seng.reset()
-        seng.set_sequences(m.draw_sequence(scfg, (args.steps + args.warmup) * cfg.num_gates)[None])
-        sgraph = seng.epoch_graph("spdhg", problem.alpha)
-        for _ in range(args.warmup):
-            sgraph.replay()
-        barrier()
-        s_ms = event_time(torch, lambda: [sgraph.replay() for _ in range(args.steps)], stream)
-        spdhg = {"value": 1000.0 * args.steps / s_ms, "unit": "epochs/s",
-                 "ms_per_epoch": s_ms / args.steps,
-                 "gpu_launches_per_epoch": 4 * cfg.num_gates + 1}
-        del seng, sgraph
+    # SPDHG of one problem does not shard (one gate per iteration): every rank runs
+    # an independent replica of the whole problem; whole-job throughput is
+    # world * K epochs over the slowest rank's device time.
+    seng = Engine([problem.operators], [problem.data])
+    seng.set_params(scfg)
+    seng.reset()
+    seng.set_sequences(m.draw_sequence(scfg, (args.steps + args.warmup) * cfg.num_gates)[None])
+    sgraph = seng.epoch_graph("spdhg", problem.alpha)
+    for _ in range(args.warmup):
+        sgraph.replay()
+    barrier()
+    s_ms = max_over_ranks(event_time(torch, lambda: [sgraph.replay() for _ in range(args.steps)],
+                                     stream))
+    spdhg = {"value": 1000.0 * args.steps * world / s_ms, "unit": "epochs/s",
+             "replicas": world, "per_replica": 1000.0 * args.steps / s_ms,
+             "ms_per_epoch": s_ms / args.steps,
+             "gpu_launches_per_epoch": 4 * cfg.num_gates + 1}
+    del seng, sgraph
 
     # ---------------- e2e through the C-ABI with host buffers ---------------
     e2e = None
@@ -712,9 +717,44 @@ def run_batch_ours(args, cfg):
     return 0
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(args) -> int | None:
+    """``--gpus N`` (N > 1) without a torch.distributed environment: start the N
+    ranks here, one process per visible GPU, through torch.distributed.run (the same
+    launch the driver uses), and return the launcher's exit code.  Returns None when
+    this process is already a rank (WORLD_SIZE set) or N == 1."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import subprocess
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if args.gpus > have:
+        print(json.dumps({"error": f"--gpus {args.gpus} needs {args.gpus} visible GPUs, "
+                                   f"found {have}", "n_gpus": args.gpus}), flush=True)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
     from paper_2410_10503_b200 import workloads
+
+    if args.impl != "reference":
+        rc = launch_ranks(args)
+        if rc is not None:
+            return rc
 
     cfg = workloads.CONFIGS[args.config]
     if args.impl == "reference":

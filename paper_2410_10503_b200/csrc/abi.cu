@@ -88,13 +88,12 @@ FwdArgs fwd_args(const mct_ray_plan* rp, const void* ws) {
     a.sp = rp->sp;
     a.jmid = rp->jmid;
     a.ws = static_cast<const char*>(ws);
-    a.item_bytes = rp->item_bytes;
+    a.wsg = rp->wsg;
     a.off_x = rp->off_x;
     a.off_xt = rp->off_xt;
     a.off_dy = rp->off_dy;
     a.off_part = rp->off_part;
     a.off_cnt = rp->off_cnt;
-    a.pair_block = rp->pair_block;
     a.off_px = rp->off_px;
     a.off_pxt = rp->off_pxt;
     a.off_pdy = rp->off_pdy;
@@ -115,16 +114,16 @@ AdjArgs adj_args(const mct_ray_plan* rp, const void* ws) {
     a.pb = rp->pb;
     a.jmid = rp->jmid;
     a.ws = static_cast<const char*>(ws);
-    a.item_bytes = rp->item_bytes;
+    a.wsg = rp->wsg;
     a.off_dy = rp->off_dy;
     a.off_img = rp->off_img;
     a.img_slot_bytes = rp->img_slot_bytes;
-    a.pair_block = rp->pair_block;
     a.off_pdy = rp->off_pdy;
     a.item0 = 0;
     a.n_items = 1;
     a.last_part = 0;
     a.asplit = 1;
+    a.kfoot = rp->kfoot;
     return a;
 }
 
@@ -136,10 +135,9 @@ PackArgs pack_args(const mct_ray_plan* rp, void* ws) {
     a.wx = rp->wx;
     a.wxt = rp->wxt;
     a.ws = static_cast<char*>(ws);
-    a.item_bytes = rp->item_bytes;
+    a.wsg = rp->wsg;
     a.off_x = rp->off_x;
     a.off_xt = rp->off_xt;
-    a.pair_block = rp->pair_block;
     a.off_px = rp->off_px;
     a.off_pxt = rp->off_pxt;
     a.x_slice_stride = (long long)rp->rows * rp->cols;
@@ -153,10 +151,9 @@ UpdArgs upd_args(const mct_ray_plan* rp, const void* ws) {
     a.rows = rp->rows;
     a.cols = rp->cols;
     a.ws = static_cast<const char*>(ws);
-    a.item_bytes = rp->item_bytes;
+    a.wsg = rp->wsg;
     a.off_img = rp->off_img;
     a.img_slot_bytes = rp->img_slot_bytes;
-    a.pair_block = rp->pair_block;
     a.asplit = 1;
     return a;
 }
@@ -236,12 +233,9 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
         adj[a].g = (float)(spacing / m);
         hmax = std::max(hmax, m / spacing);
     }
-    int K = std::max(0, (int)ceil(hmax - 1e-12) - 1);
-    if (K > 3) {
-        delete p;
-        return mct_set_error(MCT_ERR_ARG,
-                             "detector spacing below 1/4 pixel is not supported (adjoint footprint)");
-    }
+    // adjoint footprint: bins within hmax of the pixel's detector coordinate
+    // (any positive spacing, projector.py:63-68; K > 3 runs the runtime-K kernel)
+    const int K = std::max(0, (int)ceil(hmax - 1e-12) - 1);
     p->kfoot = K;
     const double hdiag = sqrt(hr * hr + hc * hc);
     int pb = (int)ceil(std::max(0.0, hdiag / spacing - p->jmid)) + K + 4;
@@ -249,16 +243,12 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     p->pb = pb;
     p->wy = num_bins + 2 * pb;
     size_t off = 0;
-    // pair-packed layouts (float2 (v[i], v[i+1] - v[i]): one load fetches both
-    // interpolation taps), two per float4 element: the item and its column
-    // mirror (X, XT), angles q and A-q (DY rows 1 .. (A-1)/2; row 0 holds the
+    // item region: the prefix every item uses (paired or not) -- A^* partial-image
+    // slots, K2 ray-split partials and arrival counters -- then the single-item
+    // (mirror) layouts: pair-packed float2 (v[i], v[i+1] - v[i]) elements, one load
+    // fetches both interpolation taps, two per float4 element: the item and its
+    // column mirror (X, XT), angles q and A-q (DY rows 1 .. (A-1)/2; row 0 holds the
     // self-paired angles 0 and A/2) -- see mct_internal.cuh
-    p->off_x = off;
-    off += align256((size_t)rows * p->wx * sizeof(float4));
-    p->off_xt = off;
-    off += align256((size_t)cols * p->wxt * sizeof(float4));
-    p->off_dy = off;
-    off += align256((size_t)(num_angles / 2 + 1) * p->wy * sizeof(float4));
     p->off_img = off;
     p->img_slot_bytes = align256((size_t)rows * cols * sizeof(float));
     // A^* partial-image slots: the largest angle split any launch of this plan may
@@ -270,7 +260,14 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     p->off_cnt = off;
     off += align256((size_t)((num_angles + MCT_FWD_ANGLES - 1) / MCT_FWD_ANGLES) *
                     ((num_bins + 31) / 32) * sizeof(int));
-    p->item_bytes = off;
+    p->wsg.pre_bytes = off;
+    p->off_x = off;
+    off += align256((size_t)rows * p->wx * sizeof(float4));
+    p->off_xt = off;
+    off += align256((size_t)cols * p->wxt * sizeof(float4));
+    p->off_dy = off;
+    off += align256((size_t)(num_angles / 2 + 1) * p->wy * sizeof(float4));
+    p->wsg.item_bytes = off;
     // gate-pair region (interleaved float4 layouts, see mct_internal.cuh)
     size_t poff = 0;
     p->off_px = poff;
@@ -279,8 +276,8 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     poff += align256((size_t)cols * p->wxt * sizeof(float4));
     p->off_pdy = poff;
     poff += align256((size_t)num_angles * p->wy * sizeof(float4));
-    p->pair_bytes = poff;
-    p->pair_block = 2 * p->item_bytes + p->pair_bytes;
+    p->wsg.pair_bytes = poff;
+    p->wsg.pair_block = poff + 2 * p->wsg.pre_bytes;
 
     cudaError_t e = cudaMalloc(&p->d_fwd, sizeof(RayAngle) * num_angles);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_adj, sizeof(AdjAngle) * num_angles);
@@ -308,7 +305,7 @@ int mct_ray_plan_destroy(mct_ray_plan* plan) {
 
 size_t mct_ray_workspace_bytes(const mct_ray_plan* plan, int batch) {
     if (!plan || batch < 1) return 0;
-    return mct_ws_bytes(plan, batch);
+    return mct_ws_bytes(plan->wsg, batch);
 }
 
 int mct_ray_forward(const mct_ray_plan* rp, const float* x, float* sino, int batch, void* ws,
@@ -577,7 +574,7 @@ int mct_family_set_params(mct_family* fam, const double* sigmas, const double* p
 
 size_t mct_family_workspace_bytes(const mct_family* fam, int items) {
     if (!fam || items < 1) return 0;
-    return mct_ws_bytes(fam->ray, items);
+    return mct_ws_bytes(fam->ray->wsg, items);
 }
 
 int mct_gated_forward(const mct_family* fam, int slice, int gate, const float* x, float* sino,

@@ -15,10 +15,9 @@
 // one fixed-point walk / one set of tent weights drives both items, and one
 // 16-byte load fetches both items' pair-packed taps from a pair region in which
 // the two items' X2 / XT2 / DY2 are interleaved element by element (float4 =
-// (item 2p pair, item 2p+1 pair)).  Items are stored in pair blocks
-//   [item 2p | item 2p+1 | pair region p]   (stride pair_block)
-// so the single-item regions (single-gate SPDHG, standalone operators) and the
-// pair regions never overlap and each keeps its own zero pads.
+// (item 2p pair, item 2p+1 pair)).  Single-item regions (single-gate SPDHG,
+// standalone operators, an odd last item) and pair regions never overlap and each
+// keeps its own zero pads (workspace layout: see mct_item_off below).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -59,6 +58,12 @@ struct AdjAngle {
 #define MCT_ASPLIT_MIN_PAIRS 8
 #endif
 
+struct WsGeom {
+    size_t item_bytes;  // a single region
+    size_t pre_bytes;   // IMG slots + K2 partials + counters (prefix of an item region)
+    size_t pair_bytes;  // interleaved X / XT / DY of a gate pair
+    size_t pair_block;  // pair_bytes + 2 * pre_bytes
+};
 struct mct_ray_plan {
     int rows, cols, A, B;
     double sp, jmid;     // detector spacing, (B-1)/2
@@ -67,8 +72,9 @@ struct mct_ray_plan {
     int kfoot;           // extra footprint bins for the adjoint (0 when sp >= step^-1)
     RayAngle* d_fwd;
     AdjAngle* d_adj;
-    size_t off_x, off_xt, off_dy, off_img, img_slot_bytes, off_part, off_cnt, item_bytes;
-    size_t off_px, off_pxt, off_pdy, pair_bytes, pair_block;  // pair region (see top)
+    size_t off_x, off_xt, off_dy, off_img, img_slot_bytes, off_part, off_cnt;
+    size_t off_px, off_pxt, off_pdy;  // pair region (see top)
+    WsGeom wsg;                       // workspace layout (see mct_item_off)
     int ksplit1;  // K2 ray split of single-gate launches (see MCT_KSPLIT_MIN)
 };
 
@@ -110,19 +116,29 @@ __host__ __device__ __forceinline__ int mct_pair_items(int items, int last_part)
 // [1, 1 + P/2), part 2 = pairs q in [1 + P/2, P + 1), P = (A-1)/2.
 __host__ __device__ __forceinline__ int mct_half_q(int A) { return 1 + ((A - 1) / 2) / 2; }
 
-// Byte offset of item `item`'s region and of pair p's region in a workspace.
-__host__ __device__ __forceinline__ size_t mct_item_off(int item, size_t item_bytes,
-                                                        size_t pair_block) {
-    return (size_t)(item >> 1) * pair_block + (size_t)(item & 1) * item_bytes;
+// Workspace layout (one per launch family; every region keeps one role for every
+// launch size, so pads zeroed once stay zero):
+//   [single region 0 | single region 1 | pair block 0 | pair block 1 | ...]
+// A single region (item_bytes) is the full item layout (IMG slots, K2 partials and
+// arrival counters, then X / XT / DY of the mirror kernels) of an unpaired item:
+// unpaired item k of a launch (k = item - pair_items, at most two: an odd last item
+// and / or a half item) uses single region k.  Pair block p is the interleaved pair
+// region (X / XT / DY of items 2p, 2p+1, pair_bytes) followed by the two items'
+// *prefixes* (pre_bytes: IMG slots, partials, counters) -- paired items never touch
+// the single-item X / XT / DY, so they hold no copy of them.
+__host__ __device__ __forceinline__ size_t mct_pair_off(int pair, const WsGeom& g) {
+    return 2 * g.item_bytes + (size_t)pair * g.pair_block;
 }
-__host__ __device__ __forceinline__ size_t mct_pair_off(int pair, size_t item_bytes,
-                                                        size_t pair_block) {
-    return (size_t)pair * pair_block + 2 * item_bytes;
+// Byte offset of item `item`'s region (paired: its prefix) in a launch whose
+// items [0, pair_items) run the gate-pair kernels.
+__host__ __device__ __forceinline__ size_t mct_item_off(int item, int pair_items,
+                                                        const WsGeom& g) {
+    return item < pair_items ? mct_pair_off(item >> 1, g) + g.pair_bytes + (item & 1) * g.pre_bytes
+                             : (size_t)(item - pair_items) * g.item_bytes;
 }
 // Workspace bytes for launches of up to `items` items.
-inline size_t mct_ws_bytes(const mct_ray_plan* p, int items) {
-    return items <= 1 ? p->item_bytes
-                      : (size_t)(items / 2) * p->pair_block + (size_t)(items & 1) * p->item_bytes;
+inline size_t mct_ws_bytes(const WsGeom& g, int items) {
+    return items <= 1 ? g.item_bytes : 2 * g.item_bytes + (size_t)(items / 2) * g.pair_block;
 }
 
 // --------------------------------------------------------------- warp plan --
@@ -185,8 +201,9 @@ __device__ __forceinline__ void resolve_item(const ItemSel& s, int item, int& sl
 struct PackArgs {
     int rows, cols, wx, wxt;
     char* ws;
-    size_t item_bytes, off_x, off_xt;
-    size_t pair_block, off_px, off_pxt;
+    WsGeom wsg;
+    size_t off_x, off_xt;
+    size_t off_px, off_pxt;
     int pair_items;          // items below this write the interleaved pair region
     ItemSel sel;
     int N;
@@ -204,8 +221,9 @@ struct FwdArgs {
     int A, B, rows, cols, wx, wxt;
     double sp, jmid;
     const char* ws;
-    size_t item_bytes, off_x, off_xt, off_dy, off_part, off_cnt;
-    size_t pair_block, off_px, off_pxt, off_pdy;
+    WsGeom wsg;
+    size_t off_x, off_xt, off_dy, off_part, off_cnt;
+    size_t off_px, off_pxt, off_pdy;
     int item0;               // first item of the launch
     int n_items;             // items of the whole call (the last may be a half item)
     int ksplit;
@@ -228,17 +246,20 @@ struct AdjArgs {
     int A, B, rows, cols, wy, pb;
     double jmid;
     const char* ws;
-    size_t item_bytes, off_dy, off_img, img_slot_bytes;
-    size_t pair_block, off_pdy;
+    WsGeom wsg;
+    size_t off_dy, off_img, img_slot_bytes;
+    size_t off_pdy;
     int item0;               // first item of the launch
     int n_items, last_part;  // items of the whole call; see ItemSel::last_part
     int asplit;
+    int kfoot;               // adjoint footprint (bins thi-kfoot .. thi+kfoot+1)
 };
 
 struct UpdArgs {
     int rows, cols;
     const char* ws;
-    size_t item_bytes, off_img, img_slot_bytes, pair_block;
+    WsGeom wsg;
+    size_t off_img, img_slot_bytes;
     int asplit;
     const float* img_override;  // plain D^* of a caller image (single item)
     ItemSel sel;

@@ -72,8 +72,8 @@ __global__ void __launch_bounds__(THREADS, MINB) pack_kernel(PackArgs p) {
     // item.  Single-item (mirror) mode: slot 0 holds W, slot 1 the column mirror
     // Wm[r][c] = W[r][cols-1-c] (X) / XT[cols-1-c] (XT) of the item's own region.
     const bool paired = item < p.pair_items;
-    char* base = paired ? p.ws + mct_pair_off(item >> 1, p.item_bytes, p.pair_block)
-                        : p.ws + mct_item_off(item, p.item_bytes, p.pair_block);
+    char* base = paired ? p.ws + mct_pair_off(item >> 1, p.wsg)
+                        : p.ws + mct_item_off(item, p.pair_items, p.wsg);
     const int s0 = paired ? (item & 1) : 0;
     float2* X = reinterpret_cast<float2*>(base + (paired ? p.off_px : p.off_x)) + 2 * MCT_PADX;
     float2* XT = reinterpret_cast<float2*>(base + (paired ? p.off_pxt : p.off_xt)) + 2 * MCT_PADX;
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(THREADS, MINB) pack_kernel(PackArgs p) {
 // paired items into their slot of the pair region (row a), single items into
 // the mirror layout of their own region (row / slot of mir_row_slot).
 __global__ void pad_sino_kernel(const float* __restrict__ sino, const AdjAngle* __restrict__ ang,
-                                char* ws, size_t item_bytes, size_t pair_block, size_t off_dy1,
+                                char* ws, WsGeom wsg, size_t off_dy1,
                                 size_t off_dy2, int A, int B, int wy, int pb, int pair_items) {
     const int item = blockIdx.z;
     const bool paired = item < pair_items;
@@ -144,8 +144,8 @@ __global__ void pad_sino_kernel(const float* __restrict__ sino, const AdjAngle* 
     int row = a, slot = item & 1;
     if (!paired) mir_row_slot(a, A, row, slot);
     float* DY = reinterpret_cast<float*>(
-                    ws + (paired ? mct_pair_off(item >> 1, item_bytes, pair_block)
-                                 : mct_item_off(item, item_bytes, pair_block)) +
+                    ws + (paired ? mct_pair_off(item >> 1, wsg)
+                                 : mct_item_off(item, pair_items, wsg)) +
                     (paired ? off_dy2 : off_dy1)) + 2 * slot;
     const float* s = sino + ((long long)item * A + a) * B;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x) {
@@ -246,8 +246,9 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
     const int jj = active ? j : p.B - 1;  // idle lanes shadow the last bin (no store)
     const RayAngle ra = p.ang[a];
     const int item0 = MIR ? p.item0 + group : G * group;  // pair launches start at item 0
-    const char* base0 = p.ws + mct_item_off(item0, p.item_bytes, p.pair_block);  // counters
-    const char* tb = MIR ? base0 : p.ws + mct_pair_off(group, p.item_bytes, p.pair_block);
+    const int np = mct_pair_items(p.n_items, p.sel.last_part);  // paired items of the call
+    const char* base0 = p.ws + mct_item_off(item0, np, p.wsg);  // counters
+    const char* tb = MIR ? base0 : p.ws + mct_pair_off(group, p.wsg);
     const int cd = ra.cols_dom;
     // tap index = hi(fx) >= 0: the row pad is folded into fx so the address is one
     // unsigned 32x64 multiply-add
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
                 if (h == 0 || pair1) {
                     double* PART = reinterpret_cast<double*>(
                         const_cast<char*>(p.ws) +
-                        mct_item_off(ray_item(h), p.item_bytes, p.pair_block) + p.off_part);
+                        mct_item_off(ray_item(h), np, p.wsg) + p.off_part);
                     PART[((long long)part * p.A + ray_angle(h)) * p.B + j] = tot[h];
                 }
             }
@@ -427,7 +428,7 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
         for (int h = 0; h < G; ++h) {
             if (h == 0 || pair1) {
                 const double* PART = reinterpret_cast<const double*>(
-                    p.ws + mct_item_off(ray_item(h), p.item_bytes, p.pair_block) + p.off_part);
+                    p.ws + mct_item_off(ray_item(h), np, p.wsg) + p.off_part);
                 double acc = 0.0;
                 for (int q = 0; q < ks; ++q)
                     acc += __ldcg(PART + ((long long)q * p.A + ray_angle(h)) * p.B + j);
@@ -525,7 +526,7 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
 template <int K, int G>
 __device__ __forceinline__ void adj_tap2(const float4* __restrict__ DY2, unsigned tlo, int thi,
                                          int delta, float g32, float omg, float* acc_a,
-                                         float* acc_b) {
+                                         float* acc_b, int kr) {
     const float F = (float)tlo;
     if (K == 0 && G == 1) {
         const float4 v = __ldg(DY2 + (unsigned)thi);
@@ -547,7 +548,7 @@ __device__ __forceinline__ void adj_tap2(const float4* __restrict__ DY2, unsigne
         const float d = F * INV_2_32;
         const float g = g32 * 4294967296.0f;
 #pragma unroll
-        for (int mm = -K; mm <= K; mm += 2) {
+        for (int mm = -(K >= 0 ? K : kr); mm <= (K >= 0 ? K : kr); mm += 2) {
             const float wa = __saturatef(fmaf(-fabsf((float)mm - d), g, 1.0f));
             const float wb = __saturatef(fmaf(-fabsf((float)(mm + 1) - d), g, 1.0f));
             if (G == 1) {
@@ -571,7 +572,7 @@ __device__ __forceinline__ void adj_tap2(const float4* __restrict__ DY2, unsigne
 // both items' pairs.
 template <int K, int G>
 __device__ __forceinline__ void adj_tap1(const float4* __restrict__ DY2, unsigned tlo, int thi,
-                                         int slot, float g32, float omg, float* acc) {
+                                         int slot, float g32, float omg, float* acc, int kr) {
     const float F = (float)tlo;
     if (K == 0) {
         const float4 v = __ldg(DY2 + (unsigned)thi);
@@ -586,7 +587,7 @@ __device__ __forceinline__ void adj_tap1(const float4* __restrict__ DY2, unsigne
         const float d = F * INV_2_32;
         const float g = g32 * 4294967296.0f;
 #pragma unroll
-        for (int mm = -K; mm <= K; mm += 2) {
+        for (int mm = -(K >= 0 ? K : kr); mm <= (K >= 0 ? K : kr); mm += 2) {
             const float4 v = __ldg(DY2 + (thi + mm));
             const float wa = __saturatef(fmaf(-fabsf((float)mm - d), g, 1.0f));
             const float wb = __saturatef(fmaf(-fabsf((float)(mm + 1) - d), g, 1.0f));
@@ -657,8 +658,9 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
     const double u0 = (double)r0 - 0.5 * (double)(p.rows - 1);
     const double v0 = (double)c0 - 0.5 * (double)(p.cols - 1);
     const int item0 = p.item0 + G * group;  // G = 2: item0 is even
-    const char* tb = G == 1 ? p.ws + mct_item_off(item0, p.item_bytes, p.pair_block)
-                            : p.ws + mct_pair_off(item0 >> 1, p.item_bytes, p.pair_block);
+    const int np = mct_pair_items(p.n_items, p.last_part);  // paired items of the call
+    const char* tb = G == 1 ? p.ws + mct_item_off(item0, np, p.wsg)
+                            : p.ws + mct_pair_off(item0 >> 1, p.wsg);
     const V* __restrict__ DY2 = reinterpret_cast<const V*>(tb + (G == 1 ? p.off_dy : p.off_pdy));
     const long long row_off = (long long)rbase;
 
@@ -684,8 +686,8 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
                 float acc[G], accm[G];
 #pragma unroll
                 for (int h = 0; h < G; ++h) acc[h] = accm[h] = 0.0f;
-                adj_tap1<K, G>(DY2, (unsigned)T, (int)(T >> 32), si, g32, omg, acc);
-                adj_tap1<K, G>(DY2, (unsigned)Tm, (int)(Tm >> 32), si, g32, omg, accm);
+                adj_tap1<K, G>(DY2, (unsigned)T, (int)(T >> 32), si, g32, omg, acc, p.kfoot);
+                adj_tap1<K, G>(DY2, (unsigned)Tm, (int)(Tm >> 32), si, g32, omg, accm, p.kfoot);
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
                     s_tot[h][m][tid] += (double)acc[h];
@@ -735,8 +737,8 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
 #pragma unroll
             for (int m = 0; m < PPT; ++m) {
                 if (m < nrows) {
-                    adj_tap2<K, G>(DY2, tlo, (int)thi, delta, g32, omg, acc[m], accm[m]);
-                    adj_tap2<K, G>(DY2, mlo, (int)mhi, delta, g32, omg, accm[m], acc[m]);
+                    adj_tap2<K, G>(DY2, tlo, (int)thi, delta, g32, omg, acc[m], accm[m], p.kfoot);
+                    adj_tap2<K, G>(DY2, mlo, (int)mhi, delta, g32, omg, accm[m], acc[m], p.kfoot);
                 }
                 fx_sub(tlo, thi, (unsigned)snr, (unsigned)(snr >> 32));
                 fx_sub(mlo, mhi, (unsigned)snr, (unsigned)(snr >> 32));
@@ -754,7 +756,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
 #pragma unroll
     for (int h = 0; h < G; ++h) {
         float* IMG = reinterpret_cast<float*>(
-            const_cast<char*>(p.ws) + mct_item_off(item0 + h, p.item_bytes, p.pair_block) +
+            const_cast<char*>(p.ws) + mct_item_off(item0 + h, np, p.wsg) +
             p.off_img + (size_t)split * p.img_slot_bytes);
         for (int m = 0; m < nrows; ++m) {
             const long long row = (long long)(rt + RSTEP * m) * p.cols;
@@ -798,7 +800,7 @@ cudaError_t launch_pack(const PackArgs& a_in, int items, cudaStream_t st) {
 cudaError_t launch_pad_sino(const float* sino, const mct_ray_plan* rp, char* ws, int items,
                             cudaStream_t st) {
     dim3 block(256), grid((rp->B + 255) / 256, rp->A, items);
-    pad_sino_kernel<<<grid, block, 0, st>>>(sino, rp->d_adj, ws, rp->item_bytes, rp->pair_block,
+    pad_sino_kernel<<<grid, block, 0, st>>>(sino, rp->d_adj, ws, rp->wsg,
                                             rp->off_dy, rp->off_pdy, rp->A, rp->B, rp->wy, rp->pb,
                                             mct_pair_items(items));
     return cudaGetLastError();
@@ -1056,14 +1058,15 @@ static void launch_adj_g(const AdjArgs& a, int kfoot, int groups, cudaStream_t s
         case 0: adj_kernel<0, G><<<grid, block, 0, st>>>(a); break;
         case 1: adj_kernel<1, G><<<grid, block, 0, st>>>(a); break;
         case 2: adj_kernel<2, G><<<grid, block, 0, st>>>(a); break;
-        default: adj_kernel<3, G><<<grid, block, 0, st>>>(a); break;
+        case 3: adj_kernel<3, G><<<grid, block, 0, st>>>(a); break;
+        default: adj_kernel<-1, G><<<grid, block, 0, st>>>(a); break;  // runtime footprint
     }
 }
 
 // Pairs first, then an odd last item on its own; both launches use the caller's
 // angle split (K4 sums the same number of partial slots for every item).
 cudaError_t launch_adj(const AdjArgs& a_in, int kfoot, int items, cudaStream_t st) {
-    if (kfoot < 0 || kfoot > 3) return cudaErrorInvalidValue;
+    if (kfoot < 0) return cudaErrorInvalidValue;
     const int np = mct_pair_items(items, a_in.last_part);
     auto pairs = [&](cudaStream_t s) {
         AdjArgs a = a_in;

@@ -17,7 +17,11 @@ namespace {
 #define K4_MINB1 0  // single-lane (single-gate) launches: compiler default
 #endif
 #ifndef K4_MINB
-#define K4_MINB 6  // register cap 42: more resident warps for the CSR gathers (C3 PDHG K4 94 -> 86 us)
+// gate-lane launches (blocks of 32 x K4_LANES threads): K4_MINB resident blocks of
+// that size, i.e. 12 x 128 = 1536 threads per SM -> a 40-register cap (the
+// allocation granularity rounds 65536 / 1536 down): more resident warps for the
+// CSR gathers (C3 PDHG K4 94 -> 86 us)
+#define K4_MINB 12
 #endif
 // K4 — one thread per pixel q of one slice (blockIdx.y): sums D_g^* img_k over
 // the slice's items in a fixed order (deterministic), then
@@ -29,7 +33,8 @@ namespace {
 // sums in lane order (fixed association: deterministic), so the per-pixel gate
 // chains run LANES-wide in parallel instead of one after the other.
 template <int MODE, int LANES>
-__global__ void __launch_bounds__(256, LANES > 1 ? K4_MINB : K4_MINB1) update_kernel(UpdArgs p) {
+__global__ void __launch_bounds__(LANES > 1 ? 32 * LANES : 256, LANES > 1 ? K4_MINB : K4_MINB1)
+update_kernel(UpdArgs p) {
     const int slice = blockIdx.y;
     const long long n = (long long)p.rows * p.cols;
     const int lane = LANES > 1 ? (int)threadIdx.y : 0;
@@ -43,13 +48,15 @@ __global__ void __launch_bounds__(256, LANES > 1 ? K4_MINB : K4_MINB1) update_ke
     const float z0 = MODE == 1 && lane == 0 ? p.z[o] : 0.0f;
     const float xn = MODE != 0 && lane == 0 ? __ldg(p.x_next + o) : 0.0f;
     float sum = 0.0f, wsum = 0.0f;
+    // paired items of the K3 launch whose partial images this gathers
+    const int np = mct_pair_items(p.sel.ips * p.sel.num_slices, p.sel.last_part);
     for (int k = lane; k < p.sel.ips; k += LANES) {
         const int item = slice * p.sel.ips + k;
         int s_, gate, iter;
         resolve_item(p.sel, item, s_, gate, iter);
         const char* img = p.img_override
                               ? reinterpret_cast<const char*>(p.img_override)
-                              : p.ws + mct_item_off(item, p.item_bytes, p.pair_block) + p.off_img;
+                              : p.ws + mct_item_off(item, np, p.wsg) + p.off_img;
         const int asplit = p.asplit;
         const size_t slot = p.img_slot_bytes;
         // sum of the adjoint's partial-image slots, fixed order (loads four at a time)

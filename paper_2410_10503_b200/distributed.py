@@ -276,6 +276,11 @@ def run_pdhg_sharded(config, problem, group=None, exchange: str = "nccl"):
     sharded_epochs(w, config.epochs, group)
     from .solvers import _raise_status
 
-    w.check()
+    # A timed-out peer wait leaves the waiting rank's z / zbar stale, and its later
+    # partials corrupt every rank: agree on the failure collectively so that every
+    # rank raises, not only the one whose wait timed out.
+    if w.p2p is not None and w.p2p_failed_anywhere(group):
+        raise RuntimeError("p2p exchange timed out waiting for a peer's partial "
+                           "(on at least one rank); the iterate is invalid")
     _raise_status(w.engine)
     return np.asarray(w.engine.x[0].double().cpu().numpy())

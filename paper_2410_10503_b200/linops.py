@@ -278,7 +278,7 @@ def power_method(op: LinearMap, iterations: int = 100, seed: int = 0,
     if iterations < 1:
         raise ValueError("iterations must be >= 1")
     if not isinstance(op, LinearMap):
-        raise TypeError("power_method needs a device LinearMap of this package")
+        return _foreign_power_method(op, iterations, seed, rtol)
     torch = _lib.require_cuda()
     rng = np.random.default_rng(seed)
     b0 = rng.standard_normal(op.domain_shape)
@@ -307,8 +307,56 @@ def power_method(op: LinearMap, iterations: int = 100, seed: int = 0,
     return float(np.sqrt(max(rayleigh, 0.0)))
 
 
+def _foreign_power_method(op, iterations: int, seed: int, rtol: float) -> float:
+    """power_method for a map that is not one of this package's device operators
+    (any object with the reference's LinearMap contract: numpy ``apply`` /
+    ``adjoint_apply``).  The Gram applications are the foreign map's own; this only
+    sequences them with the same seeded start and stopping rule (linops.py:250-272)."""
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(tuple(op.domain_shape))
+    norm0 = float(np.linalg.norm(v))
+    if norm0 == 0.0:
+        warnings.warn("degenerate start vector; returning 0", RuntimeWarning)
+        return 0.0
+    v = v / norm0
+    lam = 0.0
+    for _ in range(iterations):
+        gv = np.asarray(op.adjoint_apply(op.apply(v)), dtype=np.float64)
+        lam_new = float(np.vdot(v, gv)) / float(np.vdot(v, v))
+        gnorm = float(np.linalg.norm(gv))
+        if gnorm == 0.0:
+            warnings.warn("power iteration degenerated to zero vector; returning 0",
+                          RuntimeWarning)
+            return 0.0
+        v = gv / gnorm
+        converged = lam_new > 0 and abs(lam_new - lam) <= rtol * lam_new
+        lam = lam_new
+        if converged:
+            break
+    return float(np.sqrt(max(lam, 0.0)))
+
+
+class _ForeignGramSum:
+    """sum_i B_i^T B_i over maps outside this package (numpy contract)."""
+
+    def __init__(self, blocks):
+        self.blocks = tuple(blocks)
+        self.domain_shape = self.range_shape = tuple(self.blocks[0].domain_shape)
+
+    def apply(self, x):
+        out = np.zeros(self.domain_shape)
+        for b in self.blocks:
+            out += np.asarray(b.adjoint_apply(b.apply(x)), dtype=np.float64)
+        return out
+
+    adjoint_apply = apply
+
+
 def stacked_norm_sq(blocks: Sequence[LinearMap], iterations: int = 100, seed: int = 0) -> float:
     """Squared norm of the row stack = lambda_max(sum_i B_i^T B_i) (linops.py:275-289)."""
+    blocks = tuple(blocks)
+    if not all(isinstance(b, LinearMap) for b in blocks):
+        return _foreign_power_method(_ForeignGramSum(blocks), iterations, seed, 1e-10)
     return power_method(GramSumMap(blocks), iterations=iterations, seed=seed)
 
 

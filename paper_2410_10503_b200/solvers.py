@@ -30,9 +30,9 @@ from typing import Callable, Sequence
 import numpy as np
 
 from . import _lib
-from .engine import Engine
-from .experiment_io import ConvergenceRecord
-from .functionals import fit_value, g_value, moduli
+from .engine import U64_MAX_AS_I64, Engine, split_operator
+from .experiment_io import ConvergenceRecord, rmse
+from .functionals import fit_value, g_value, moduli, prox_fstar, prox_g
 from .linops import LinearMap
 
 __all__ = [
@@ -111,18 +111,33 @@ class Problem:
             cache["data_objective"] = sum(fit_value(n, d, np.zeros_like(d)) for d in self.data)
         return cache["data_objective"]
 
+    ENGINE_CACHE = 2  # device engines kept per problem (LRU)
+
     def _engine(self, keep_projections: bool) -> Engine:
         """The device engine run() uses for this (immutable) problem: data, warps and
         workspace uploaded once and reused by later runs (state is reset per run).
         One engine per (device, stream), so runs issued concurrently on different
-        streams never share state."""
+        streams never share state; at most ``ENGINE_CACHE`` engines stay cached
+        (least recently used evicted; a run in flight keeps its own reference).
+
+        The data blocks are uploaded when the engine is built: like the operators,
+        ``Problem.data`` must not be modified in place after the first run()
+        (build a new Problem instead, or call ``release()``)."""
         torch = _lib.require_cuda()
-        cache = self.__dict__.setdefault("_cache", {})
+        cache = self.__dict__.setdefault("_engines", {})
         stream = torch.cuda.current_stream()
-        key = ("engine", bool(keep_projections), stream.device.index, stream.cuda_stream)
-        if key not in cache:
-            cache[key] = Engine([self.operators], [self.data], keep_projections=keep_projections)
-        return cache[key]
+        key = (bool(keep_projections), stream.device.index, stream.cuda_stream)
+        eng = cache.pop(key, None)
+        if eng is None:
+            while len(cache) >= self.ENGINE_CACHE:
+                cache.pop(next(iter(cache)))
+            eng = Engine([self.operators], [self.data], keep_projections=keep_projections)
+        cache[key] = eng  # most recently used last
+        return eng
+
+    def release(self) -> None:
+        """Drop the cached device engines (data, duals, workspace) of this problem."""
+        self.__dict__.pop("_engines", None)
 
 
 @dataclass(frozen=True)
@@ -362,6 +377,92 @@ def _raise_status(eng: Engine):
         raise DivergenceError(f"non-finite dual iterate (gate {dual[1]}) at iteration {dual[0]}")
 
 
+def fused(problem: Problem) -> bool:
+    """True when every operator of ``problem`` is a gated operator of this package
+    (RayTransform, or a ray transform composed with a warp): ``step`` / ``run`` then
+    execute the fused sm_100a iteration.  Any other map honouring the reference's
+    LinearMap contract (linops.py:39-73) runs through ``_operator_step``."""
+    try:
+        for op in problem.operators:
+            split_operator(op)
+    except TypeError:
+        return False
+    return True
+
+
+def _operator_step(state: SolverState, config: SolverConfig, problem: Problem,
+                   draw: Callable[[], tuple]) -> SolverState:
+    """One iteration over operators the fused engine does not know (solvers.py:316-366):
+    the maps' own ``apply`` / ``adjoint_apply`` (wherever those compute) sequenced
+    on float64 arrays, in the reference's order -- primal check before the draw,
+    y_i assigned gate by gate, z / zbar / x only after every gate passed."""
+    if state._engine is not None:  # a state last advanced by the fused engine
+        state._host, state._engine, state._problem = state._snapshot_host(), None, None
+    h = state._host
+    n = problem.num_gates
+    x_next = prox_g(problem.alpha, config.tau, h["x"] - config.tau * h["zbar"])
+    if not np.isfinite(x_next).all():
+        raise DivergenceError(f"non-finite primal iterate at iteration {state.iteration + 1}")
+    subset = draw()
+    while len(subset) == 0:
+        subset = draw()
+    state._last = {}
+    updates = []
+    for i in subset:
+        op, sigma = problem.operators[i], config.sigmas[i]
+        ax = np.asarray(op.apply(x_next), dtype=np.float64)
+        state.fwd_calls += 1
+        state._last[i] = ax
+        y_next = prox_fstar(n, problem.data[i], sigma, h["y"][i] + sigma * ax)
+        if not np.isfinite(y_next).all():
+            raise DivergenceError(
+                f"non-finite dual iterate (gate {i}) at iteration {state.iteration + 1}")
+        updates.append((i, np.asarray(op.adjoint_apply(y_next - h["y"][i]), dtype=np.float64)))
+        state.adj_calls += 1
+        h["y"][i] = y_next
+    for _, dz in updates:
+        h["z"] += dz
+    h["zbar"] = h["z"].copy()
+    for i, dz in updates:
+        h["zbar"] += (config.theta / config.probs[i]) * dz
+    h["x"] = x_next
+    state.iteration += 1
+    state.epoch += len(subset) / n
+    return state
+
+
+def _operator_run(config: SolverConfig, problem: Problem, saddle, truth, on_epoch):
+    """run() over operators the fused engine does not know (solvers.py:369-432)."""
+    state = SolverState.zeros(problem)
+    record = ConvergenceRecord()
+    rng = np.random.default_rng(config.seed)
+    guard = _guard(problem.data_objective())
+    n = problem.num_gates
+    for epoch_index in range(1, config.epochs + 1):
+        for _ in range(config.iterations_per_epoch):
+            _operator_step(state, config, problem,
+                           lambda: sample_gates(rng, config.probs, config.mode))
+        last = state.last_projections
+        if config.mode == "pdhg" and len(last) == n:  # reuse this epoch's projections
+            value = g_value(problem.alpha, state.x) + sum(
+                fit_value(n, problem.data[i], last[i]) for i in range(n))
+        else:
+            value = problem.objective(state.x)
+        if not math.isfinite(value) or value > guard:
+            raise DivergenceError(
+                f"objective {value:.3e} exceeded the divergence guard "
+                f"at epoch {epoch_index} (iteration {state.iteration})")
+        record.append(epoch=float(epoch_index),
+                      dist_sq=saddle.distance_sq(state.x, state.y) if saddle is not None
+                      else math.nan,
+                      objective=value,
+                      rmse_to_truth=rmse(state.x, truth) if truth is not None else math.nan,
+                      fwd_calls=state.fwd_calls, adj_calls=state.adj_calls)
+        if on_epoch is not None:
+            on_epoch(epoch_index, state)
+    return state.x.copy(), record
+
+
 def step(state: SolverState, config: SolverConfig, problem: Problem,
          draw: Callable[[], tuple]) -> SolverState:
     """Advance the state by one iteration in place (solvers.py:316-366).
@@ -369,10 +470,12 @@ def step(state: SolverState, config: SolverConfig, problem: Problem,
     ``draw`` supplies the gate subset; an empty draw is retried.  Raises
     :class:`DivergenceError` on the first non-finite iterate.
     """
-    torch = _lib.require_cuda()
     n = problem.num_gates
     if config.num_gates != n:
         raise ValueError("config and problem disagree on the gate count")
+    if not fused(problem):
+        return _operator_step(state, config, problem, draw)
+    torch = _lib.require_cuda()
     eng = state._bind(problem)
     eng.set_params(config)
     subset = draw()
@@ -384,8 +487,28 @@ def step(state: SolverState, config: SolverConfig, problem: Problem,
     if len(set(subset)) != len(subset):
         raise ValueError("a draw may not repeat a gate within one iteration")
     gates = torch.tensor(subset, dtype=torch.int32, device=eng.device)
+    # the fused iteration updates x, z, zbar and the drawn y_i in place: keep the
+    # pre-step values so that a DivergenceError leaves the state where the
+    # reference's would be (it raises before assigning x, z and the failing y_i)
+    saved = [t.clone() for t in (eng.x, eng.z, eng.zbar)] + [eng.y[0, i].clone() for i in subset]
     eng.iteration(eng.items_subset(gates, len(subset), state.iteration + 1), problem.alpha)
-    _raise_status(eng)
+    primal, dual = eng.read_status()
+    if primal is not None or dual is not None:
+        for t, v in zip((eng.x, eng.z, eng.zbar), saved[:3]):
+            t.copy_(v)
+        # a dual failure at subset position k: gates before k keep their new y_i
+        # (solvers.py:341-358 assigns y_i gate by gate); the primal check fails first
+        k = 0 if primal is not None else subset.index(dual[1])
+        for pos in range(k, len(subset)):
+            eng.y[0, subset[pos]].copy_(saved[3 + pos])
+        if primal is None:
+            state.fwd_calls += k + 1
+            state.adj_calls += k
+            state.last_projections = {i: None for i in subset[:k + 1]}
+        try:
+            _raise_status(eng)
+        finally:
+            eng.status.fill_(U64_MAX_AS_I64)
     state.fwd_calls += len(subset)
     state.adj_calls += len(subset)
     state.last_projections = {i: None for i in subset}
@@ -414,6 +537,8 @@ def run(config: SolverConfig, problem: Problem, saddle: SaddlePoint | None = Non
     """
     if config.num_gates != problem.num_gates:
         raise ValueError("config and problem disagree on the gate count")
+    if not fused(problem):
+        return _operator_run(config, problem, saddle, truth, on_epoch)
     record = ConvergenceRecord()
     if config.epochs == 0:
         return np.zeros(problem.image_shape), record

@@ -54,3 +54,16 @@ def test_our_arm_json_line(config):
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert line["gpu_launches"] >= 4 * line["steps"]
     assert "sm_mhz" in line["clocks"] and "workload" in line["config"]
+
+
+def test_gpus_beyond_visible_devices_fails_clearly():
+    """--gpus N starts N ranks itself; with fewer visible GPUs it refuses (rc 2) with a
+    one-line JSON reason instead of silently timing one rank."""
+    import torch
+
+    n = max(2, torch.cuda.device_count() + 1)
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", str(n), "--steps", "1",
+                          "--warmup", "3"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 2, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert "error" in line and line["n_gpus"] == n

@@ -1,0 +1,181 @@
+"""GPU tier: K-epoch trajectory parity at the BASELINE bench configurations.
+
+north_star: "Iterates after K epochs must agree within relative L2 1e-3 for the
+same sampling seed" -- here on the exact bench path (``bench.py``): the full-size
+C2 / C3 / C4 / C5 workloads, step sizes from the device power method (the rule
+bench.py uses), the fused K1..K4 launches through ``Engine`` (20- and 40-item
+gate-pair launches for PDHG, single-gate mirror launches for SPDHG, S-slice
+launches for the C5 batch), replayed as a captured epoch graph and eagerly.
+The checker is the fp64 oracle (oracle/, reference solvers.py:316-419) run with
+the identical SolverConfig.
+
+Non-vacuity: the reference starts from zeros and x+ = prox(x - tau*zbar), so one
+PDHG epoch leaves x == 0 (reference test_solvers.py:289).  Every comparison here
+asserts ||reference|| > 0 first, runs >= 2 PDHG epochs, and also compares z
+(the aggregate A^* y, nonzero after the first epoch) and the duals y_i.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import solver as osolver
+
+pytestmark = pytest.mark.gpu
+
+ITER_TOL = 1e-3  # north_star: relative L2 after K epochs
+
+
+def strict_rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    den = float(np.linalg.norm(b))
+    assert den > 0.0, "reference iterate is zero: the comparison would be vacuous"
+    return float(np.linalg.norm(a - b)) / den
+
+
+def stacked_rel(ys, yrefs):
+    num = sum(float(np.linalg.norm(np.asarray(a, np.float64) - b) ** 2) for a, b in zip(ys, yrefs))
+    den = sum(float(np.linalg.norm(b) ** 2) for b in yrefs)
+    assert den > 0.0
+    return (num / den) ** 0.5
+
+
+@pytest.fixture(scope="module")
+def m():
+    import paper_2410_10503_b200 as m
+
+    m.build_native()
+    return m
+
+
+def bench_problem(m, name, slice_index=0):
+    """The bench's problem and step-size inputs (bench.build_problem)."""
+    from paper_2410_10503_b200 import workloads
+
+    cfgw = workloads.CONFIGS[name]
+    problem, truth, inp = m.simulate.workload_problem(cfgw, slice_index)
+    return cfgw, problem, inp
+
+
+def bench_norms(m, problem, stacked=True):
+    norms = [m.power_method(op, iterations=20, seed=0) for op in problem.operators]
+    s = m.stacked_norm_sq(problem.operators, iterations=20, seed=0) if stacked else None
+    return norms, s
+
+
+def oracle_ops(cfgw, inp):
+    return oracle.gate_operators(oracle.Geometry(*cfgw.geometry_args), inp.gates,
+                                 threads=oracle.default_threads())
+
+
+def run_capture(m, cfg, problem, graph):
+    """run() on the device; returns (x, z, y) of the final epoch (float64)."""
+    seen = {}
+
+    def grab(e, st):
+        if e == cfg.epochs:
+            seen["z"] = st.z
+            seen["y"] = st.y
+
+    x, _ = m.run(cfg, problem, graph=graph, diagnostics=False, on_epoch=grab)
+    return x, seen["z"], seen["y"]
+
+
+def check_state(x, z, y, ost, label):
+    ex = strict_rel(x, ost.x)
+    ez = strict_rel(z, ost.z)
+    ey = stacked_rel(y, ost.y)
+    assert ex <= ITER_TOL, f"{label}: x rel L2 {ex:.3e}"
+    assert ez <= ITER_TOL, f"{label}: z rel L2 {ez:.3e}"
+    assert ey <= ITER_TOL, f"{label}: y rel L2 {ey:.3e}"
+    return ex, ez, ey
+
+
+def test_c3_pdhg_5_epochs_bench_path_vs_oracle(m):
+    """C3 (512^2, 20 dense gates, 720x729): 5 PDHG epochs, 20-item gate-pair launches,
+    as the bench's epoch graph and eagerly, vs the fp64 oracle."""
+    cfgw, problem, inp = bench_problem(m, "c3")
+    norms, stacked = bench_norms(m, problem)
+    epochs = 5
+    cfg = m.default_config("pdhg", norms, cfgw.alpha, epochs, stacked_norm_sq=stacked)
+    ocfg = osolver.default_config("pdhg", norms, cfgw.alpha, epochs, stacked_norm_sq=stacked)
+    assert (cfg.sigmas, cfg.tau) == (ocfg.sigmas, ocfg.tau)
+    ost, _ = osolver.run(ocfg, cfgw.alpha, oracle_ops(cfgw, inp), list(problem.data),
+                         diagnostics=False)
+    assert np.linalg.norm(ost.x) > 0
+    xg, zg, yg = run_capture(m, cfg, problem, graph=True)
+    xe, ze, ye = run_capture(m, cfg, problem, graph=False)
+    check_state(xg, zg, yg, ost, "graph")
+    check_state(xe, ze, ye, ost, "eager")
+    assert np.array_equal(xg, xe)  # graph replay == eager launches, bit for bit
+
+
+def test_c3_spdhg_2_epochs_vs_oracle(m):
+    """C3 SPDHG: 40 single-gate iterations (mirror-angle K2/K3, the bench's SPDHG
+    epoch graph) with the reference's seeded gate sequence."""
+    cfgw, problem, inp = bench_problem(m, "c3")
+    norms, _ = bench_norms(m, problem, stacked=False)
+    epochs = 2
+    cfg = m.default_config("spdhg", norms, cfgw.alpha, epochs, seed=0)
+    ocfg = osolver.default_config("spdhg", norms, cfgw.alpha, epochs, seed=0)
+    ost, _ = osolver.run(ocfg, cfgw.alpha, oracle_ops(cfgw, inp), list(problem.data),
+                         diagnostics=False)
+    assert np.linalg.norm(ost.x) > 0
+    x, z, y = run_capture(m, cfg, problem, graph=True)
+    check_state(x, z, y, ost, "c3 spdhg")
+
+
+def test_c4_pdhg_2_epochs_vs_oracle(m):
+    """C4 (1024^2, 40 dense gates, 1440x1453): 2 PDHG epochs (40-item launches) vs the
+    oracle with on-the-fly Joseph weights (the reference cannot hold C4's tables)."""
+    cfgw, problem, inp = bench_problem(m, "c4")
+    norms, stacked = bench_norms(m, problem)
+    epochs = 2
+    cfg = m.default_config("pdhg", norms, cfgw.alpha, epochs, stacked_norm_sq=stacked)
+    ocfg = osolver.default_config("pdhg", norms, cfgw.alpha, epochs, stacked_norm_sq=stacked)
+    ost, _ = osolver.run(ocfg, cfgw.alpha, oracle_ops(cfgw, inp), list(problem.data),
+                         diagnostics=False)
+    assert np.linalg.norm(ost.x) > 0
+    x, z, y = run_capture(m, cfg, problem, graph=True)
+    check_state(x, z, y, ost, "c4 pdhg")
+
+
+def test_c5_batch_slices_vs_per_slice_oracle(m):
+    """C5 (512^2 slices, 10 dense gates, 720x729, alpha 1e-2): 4 full-size slices
+    solved in one batched launch (blockIdx.z = slice, the bench's C5 path), SPDHG with
+    per-slice sampling seeds, vs one oracle run per slice."""
+    from paper_2410_10503_b200 import workloads
+
+    cfgw = workloads.CONFIGS["c5"]
+    S, epochs = 4, 2
+    probs, inps = [], []
+    for s in range(S):
+        p, _, inp = m.simulate.workload_problem(cfgw, s)
+        probs.append(p)
+        inps.append(inp)
+    # the bench's C5 step-size rule: slice 0's norms x 1.1 for every slice
+    norms = [1.1 * m.power_method(op, iterations=20, seed=0) for op in probs[0].operators]
+    cfgs = [m.default_config("spdhg", norms, cfgw.alpha, epochs, seed=cfgw.seed + s)
+            for s in range(S)]
+    out = m.run_batch(cfgs, probs)
+    for s in range(S):
+        ocfg = osolver.default_config("spdhg", norms, cfgw.alpha, epochs, seed=cfgw.seed + s)
+        ost, _ = osolver.run(ocfg, cfgw.alpha, oracle_ops(cfgw, inps[s]), list(probs[s].data),
+                             diagnostics=False)
+        e = strict_rel(out[s][0], ost.x)
+        assert e <= ITER_TOL, f"slice {s}: x rel L2 {e:.3e}"
+
+
+def test_c2_spdhg_50_epochs_vs_oracle(m):
+    """C2 (256^2, 10 dense gates, 360x363): the full 50-epoch SPDHG budget of BASELINE."""
+    cfgw, problem, inp = bench_problem(m, "c2")
+    norms, _ = bench_norms(m, problem, stacked=False)
+    cfg = m.default_config("spdhg", norms, cfgw.alpha, cfgw.epochs, seed=cfgw.seed)
+    ocfg = osolver.default_config("spdhg", norms, cfgw.alpha, cfgw.epochs, seed=cfgw.seed)
+    assert cfgw.epochs == 50
+    ost, objs = osolver.run(ocfg, cfgw.alpha, oracle_ops(cfgw, inp), list(problem.data))
+    x, z, y = run_capture(m, cfg, problem, graph=True)
+    check_state(x, z, y, ost, "c2 spdhg")
+    _, rec = m.run(cfg, problem)  # diagnostics on: the per-epoch objective column
+    assert np.allclose(rec.objective, objs, rtol=ITER_TOL)

@@ -322,9 +322,29 @@ def test_edge_geometries_vs_oracle(m, g):
         assert rel_l2(ab[i], orc.adjoint_apply(yb[i].astype(np.float64))) <= TOL, i
 
 
-def test_too_fine_detector_rejected(m):
-    with pytest.raises(ValueError, match="spacing"):
-        m.RayTransform(m.Geometry(32, 32, 8, 400, 0.1)).apply(np.zeros((32, 32)))
+@pytest.mark.parametrize("g", [(32, 32, 8, 400, 0.1), (48, 40, 30, 301, 0.2),
+                               (33, 33, 12, 150, 0.24), (64, 64, 9, 2000, 0.05)])
+def test_fine_detector_spacing_vs_oracle(m, g):
+    """Any positive detector spacing (projector.py:63-68): below 1/4 pixel the A^*
+    footprint exceeds the unrolled kernels (K > 3) and the runtime-footprint kernel
+    runs; single items, a batch of 3 (gate pair + odd item) and the adjoint
+    identity against the fp64 oracle."""
+    import torch
+
+    r = np.random.default_rng(int(g[3]))
+    geom = m.Geometry(*g)
+    op = m.RayTransform(geom)
+    orc = oracle.RayTransform(oracle.Geometry(*g))
+    x = r.standard_normal(geom.image_shape).astype(np.float32).astype(np.float64)
+    y = r.standard_normal(geom.sino_shape).astype(np.float32).astype(np.float64)
+    assert rel_l2(op.apply(x), orc.apply(x)) <= TOL
+    assert rel_l2(op.adjoint_apply(y), orc.adjoint_apply(y)) <= TOL
+    lhs, rhs = float(np.vdot(op.apply(x), y)), float(np.vdot(x, op.adjoint_apply(y)))
+    assert abs(lhs - rhs) <= 1e-5 * max(abs(lhs), abs(rhs))
+    yb = r.standard_normal((3,) + tuple(geom.sino_shape)).astype(np.float32)
+    ab = op.adjoint_batch(torch.from_numpy(yb).cuda()).double().cpu().numpy()
+    for i in range(3):
+        assert rel_l2(ab[i], orc.adjoint_apply(yb[i].astype(np.float64))) <= TOL, i
 
 
 def test_dense_zero_field_is_identity_and_out_of_frame(m, rng):
@@ -391,7 +411,8 @@ def test_gated_forward_many_matches_single(m, rng):
 
 
 @pytest.mark.parametrize("g", [(1, 1, 1, 1, 1.0), (7, 3, 5, 4, 0.8), (40, 1, 6, 45, 1.0),
-                               (32, 32, 7, 200, 0.3), (65, 66, 48, 95, 1.0)])
+                               (32, 32, 7, 200, 0.3), (65, 66, 48, 95, 1.0),
+                               (24, 24, 6, 400, 0.08)])
 def test_no_writes_outside_buffers(m, g):
     """Out-of-bounds write check without a sanitizer: workspace and outputs carry
     canary tails (0xAB) that every launch must leave intact, and a second

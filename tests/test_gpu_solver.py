@@ -297,43 +297,6 @@ def test_p2p_exchange_matches_nccl_single_rank(m, golden_tiny):
         dist.destroy_process_group()
 
 
-def test_c2_shape_spdhg_trajectory_vs_oracle(m):
-    """BASELINE C2 shape (256^2, 10 dense gates, 360x363): 2 SPDHG epochs vs the oracle."""
-    from paper_2410_10503_b200 import workloads
-
-    cfgw = workloads.CONFIGS["c2"]
-    problem, truth, inp = m.simulate.workload_problem(cfgw, 0)
-    norms = [m.power_method(op, iterations=20) for op in problem.operators]
-    cfg = m.default_config("spdhg", norms, cfgw.alpha, 2, seed=3)
-    x, rec = m.run(cfg, problem, diagnostics=False)
-    oops = oracle.gate_operators(oracle.Geometry(*cfgw.geometry_args), inp.gates,
-                                 threads=oracle.default_threads())
-    ocfg = osolver.default_config("spdhg", norms, cfgw.alpha, 2, seed=3)
-    st, _ = osolver.run(ocfg, cfgw.alpha, oops, [np.asarray(d) for d in problem.data],
-                        diagnostics=False)
-    assert rel_l2(x, st.x) <= ITER_TOL
-
-
-def test_c3_pdhg_epoch_vs_oracle(m):
-    """BASELINE C3 at full size (512^2, 20 dense gates, 720x729): one PDHG epoch of
-    the bench workload vs the fp64 oracle, identical step sizes."""
-    from paper_2410_10503_b200 import workloads
-
-    cfgw = workloads.CONFIGS["c3"]
-    problem, truth, inp = m.simulate.workload_problem(cfgw, 0)
-    norm = float(np.sqrt(0.966 * cfgw.num_angles * cfgw.n))  # SURVEY §8d estimate
-    cfg = m.default_config("pdhg", [norm] * cfgw.num_gates, cfgw.alpha, 1,
-                           stacked_norm_sq=cfgw.num_gates * norm ** 2)
-    x, rec = m.run(cfg, problem)
-    oops = oracle.gate_operators(oracle.Geometry(*cfgw.geometry_args), inp.gates,
-                                 threads=oracle.default_threads())
-    ocfg = osolver.default_config("pdhg", [norm] * cfgw.num_gates, cfgw.alpha, 1,
-                                  stacked_norm_sq=cfgw.num_gates * norm ** 2)
-    st, objs = osolver.run(ocfg, cfgw.alpha, oops, [np.asarray(d) for d in problem.data])
-    assert rel_l2(x, st.x) <= ITER_TOL
-    assert rec.objective[0] == pytest.approx(objs[0], rel=ITER_TOL)
-
-
 def test_cg_reference_matches_reference_saddle(m, golden_tiny):
     """Device CG saddle (solvers.py:435-490) vs the reference's fp64 CG saddle."""
     G = golden_tiny
@@ -568,3 +531,27 @@ def test_non_square_dense_trajectories_vs_oracle(m, shape, angles, bins, sp):
         st, objs = osolver.run(ocfg, 1e-2, oops, data)
         assert rel_l2(x, st.x) <= ITER_TOL, mode
         assert np.allclose(rec.objective, objs, rtol=ITER_TOL), mode
+
+
+def test_step_divergence_leaves_state_at_last_good_iterate(m, golden_tiny):
+    """solvers.py:329-352 raises before assigning x, z and the failing y_i: after a
+    DivergenceError from step() the device state still holds the pre-step iterate
+    (not x_next / the non-finite duals), and the counters did not advance."""
+    G = golden_tiny
+    problem = tiny_problem(m, G)
+    cfg = m.default_config("pdhg", np.asarray(G["gate_norms"]) / 1000.0, problem.alpha, 1)
+    st = m.SolverState.zeros(problem)
+    for _ in range(2000):
+        before = (st.x, st.z, st.zbar, st.y, st.iteration)
+        try:
+            m.step(st, cfg, problem, lambda: (0, 1, 2, 3))
+        except m.DivergenceError:
+            break
+    else:
+        pytest.fail("no divergence")
+    assert np.array_equal(st.x, before[0]) and np.array_equal(st.z, before[1])
+    assert np.array_equal(st.zbar, before[2]) and st.iteration == before[4]
+    assert all(np.isfinite(v).all() for v in (st.x, st.z, st.zbar))
+    # the iterate is still the last finite one: stepping again raises again
+    with pytest.raises(m.DivergenceError):
+        m.step(st, cfg, problem, lambda: (0, 1, 2, 3))
