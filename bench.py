@@ -145,6 +145,103 @@ def alg_bytes(cfg):
             "elem": b_elem, "min_pair": b_min_pair, "S": S}
 
 
+def joseph_samples_nz(cfg) -> int:
+    """Joseph samples with a nonzero weight in one application of A (projector.py:
+    134-166): per ray (a, j), the dominant-axis steps k whose continuous minor index
+    cont_k = P*s_j + Q + k*slope lies in (-1, lim), i.e. with at least one tap inside
+    the image.  Exact integer count from the reference's own angle / bin formulas."""
+    n_r = n_c = cfg.n
+    A, B = cfg.num_angles, cfg.num_bins
+    ang = np.arange(A) * (math.pi / A)
+    cs, sn = np.cos(ang), np.sin(ang)
+    rdom = np.abs(cs) >= sn
+    s = (np.arange(B) - (B - 1) / 2.0) * 1.0
+    hr, hc = 0.5 * (n_r - 1), 0.5 * (n_c - 1)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        P = np.where(rdom, 1.0 / cs, -1.0 / sn)
+        slope = np.where(rdom, sn / cs, cs / sn)
+    Q = np.where(rdom, hc - hr * slope, hr - hc * slope)
+    lim = np.where(rdom, n_c, n_r)[:, None].astype(np.float64)
+    nmaj = np.where(rdom, n_r, n_c)[:, None]
+    c0 = P[:, None] * s[None, :] + Q[:, None]
+    sl = slope[:, None] * np.ones((1, B))
+    flat = sl == 0.0
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ka, kb = (-1.0 - c0) / sl, (lim - c0) / sl
+    lo, hi = np.minimum(ka, kb), np.maximum(ka, kb)
+    kmin = np.maximum(0, np.floor(lo) + 1)
+    kmax = np.minimum(nmaj - 1, np.ceil(hi) - 1)
+    cnt = np.where(flat, np.where((c0 > -1.0) & (c0 < lim), nmaj, 0),
+                   np.clip(kmax - kmin + 1, 0, None))
+    return int(cnt.sum())
+
+
+def l1_operand_bytes(cfg):
+    """Bytes the K2 / K3 gathers must deliver from L1 to registers per item (fp32):
+    K2: one (value, forward difference) pair = 8 B per nonzero Joseph sample; K3: the
+    (value, difference) pair of the bin under every pixel-angle tent = 8 B per
+    pixel-angle (footprint 2 bins, spacing 1).  A gate pair fetches both items' 8 B in
+    one 16-byte load: 512 B per warp request, 4 L1 wavefronts at the ideal."""
+    return {"K2_forward_dual": 8 * joseph_samples_nz(cfg),
+            "K3_adjoint": 8 * cfg.n * cfg.n * cfg.num_angles}
+
+
+def l1_peak_gbs(sm_mhz):
+    """L1 data-pipe peak: one 128-byte wavefront per SM per clock (B200: 148 SMs)
+    at the SM clock sampled during the timed region.  tools/micro/l1_peak.cu measures
+    the delivered fraction of it for contiguous 16-byte requests
+    (profiles/l1_peak.json)."""
+    sms = 148
+    try:
+        import torch
+
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    except Exception:
+        pass
+    return 128.0 * sms * float(sm_mhz) * 1e6 / 1e9
+
+
+def roofline_line(cfg, kern_ms, items, traffic_all, wave_frac, sm_mhz, hbm_peak, peak_src):
+    """The bench line's ``roofline``: the limiter that binds K2 / K3 is the L1 data
+    pipe (ncu: LSU wavefronts 96 % / 75 % of peak, DRAM < 3 %), so the headline
+    fraction is operand bytes delivered L1 -> registers (l1_operand_bytes, exact
+    counts) over the data-pipe peak; the SURVEY §8d SpMV-equivalent HBM figure and
+    the compulsory-bytes HBM fraction are kept as labelled secondary fields.
+    ``kern_ms``: event time of each kernel summed over one step; ``items``: items
+    (gate-slices) one step's launches process."""
+    l1b = l1_operand_bytes(cfg)
+    peak = l1_peak_gbs(sm_mhz)
+    per = {}
+    for k in ("K2_forward_dual", "K3_adjoint"):
+        gbs = l1b[k] * items / (kern_ms[k] * 1e-3) / 1e9
+        per[k] = {"ms": kern_ms[k], "operand_bytes": l1b[k] * items, "achieved": gbs,
+                  "frac": gbs / peak,
+                  "l1_wavefront_frac_ncu": (wave_frac or {}).get(k),
+                  "dram_bytes_ncu": (traffic_all or {}).get(k)}
+    dominant = max(per, key=lambda k: per[k]["ms"])
+    ab = alg_bytes(cfg)
+    spmv = ab[dominant] * items / (kern_ms[dominant] * 1e-3) / 1e9
+    step_ms = sum(kern_ms.values())
+    return {
+        "bound": "l1_data_pipe", "kernel": dominant, "achieved": per[dominant]["achieved"],
+        "peak": peak, "unit": "GB/s", "frac": per[dominant]["frac"],
+        "traffic": per[dominant]["dram_bytes_ncu"],
+        "peak_source": f"128 B/clk/SM L1 data pipe x SMs x {sm_mhz:.0f} MHz (sampled SM clock); "
+                       "delivered fraction measured by tools/micro/l1_peak.cu "
+                       "(profiles/l1_peak.json)",
+        "bytes_model": "operand bytes L1 -> registers: 8 B (value, difference) per nonzero "
+                       "Joseph sample (K2) / per pixel-angle tent (K3) per item",
+        "kernels": per,
+        "hbm": {"peak": hbm_peak, "peak_source": peak_src,
+                "spmv_equivalent_gbs": spmv, "spmv_equivalent_frac": spmv / hbm_peak,
+                "spmv_note": "SURVEY §8d algorithmic bytes (4 B per nonzero); taps are "
+                             "served from L1, so this exceeds the HBM peak",
+                "compulsory_frac": ab["min_pair"] * items / (step_ms * 1e-3) / 1e9 / hbm_peak,
+                "dram_frac_ncu": (per[dominant]["dram_bytes_ncu"] / (kern_ms[dominant] * 1e-3)
+                                  / 1e9 / hbm_peak) if per[dominant]["dram_bytes_ncu"] else None},
+    }
+
+
 TRAFFIC_ITEMS = 20  # items of the launch profiles/ncu_traffic.json was captured on
 
 
@@ -394,8 +491,13 @@ def run_ours(args, cfg):
     iter_ms = sum(kern.values())
     dominant = max(("K2_forward_dual", "K3_adjoint"), key=lambda k: kern[k])
     tr = load_traffic()
+    # ncu DRAM bytes / wavefront fractions were captured on the 20-item C3 launch
+    traffic_all = ({k: v * items_per_launch / TRAFFIC_ITEMS for k, v in tr.items()
+                    if k.startswith("K")} if cfg.name == "c3" else None)
+    wave_frac = tr.get("l1_data_pipe_frac") if cfg.name == "c3" else None
     traffic = tr.get(dominant) if cfg.name == "c3" else None
     l1_frac = (tr.get("l1_data_pipe_frac") or {}).get(dominant) if cfg.name == "c3" else None
+    clk_mhz = clocks.summary()["sm_mhz"] or clocks.max_mhz or 1965.0
     if traffic is not None:  # captured on the 20-item C3 launch: scale to this launch
         traffic = traffic * items_per_launch / TRAFFIC_ITEMS
     ws_mb = (eng.ws.numel() + 4 * (eng.y.numel() + eng.d.numel() + 4 * eng.x.numel())) / 1e6
@@ -504,13 +606,8 @@ def run_ours(args, cfg):
                        "exchange": (exchange if use_dist else "none (single process)"),
                        "l2": f"per-epoch working set {ws_mb:.0f} MB (workspace + state) > "
                              f"126 MB L2: no flush needed"},
-            "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved,
-                         "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                         "traffic": traffic, "peak_source": peak_src,
-                         "bytes_model": "SpMV-equivalent algorithmic bytes, SURVEY.md §8d",
-                         "l1_data_pipe_frac": l1_frac,
-                         "limiter": "L1 data pipe (taps served from L1/L2; ncu LSU wavefronts "
-                                    "vs peak, profiles/ncu_traffic.json)"},
+            "roofline": roofline_line(cfg, kern, items_per_launch, traffic_all, wave_frac,
+                                      clk_mhz, hbm_peak, peak_src),
             "roofline_pair": {"achieved_alg_gbs": pair_gbs, "frac_alg": pair_gbs / hbm_peak,
                               "achieved_min_gbs": min_gbs, "frac_min": min_gbs / hbm_peak,
                               "joseph_samples_per_s": 2 * ab["S"] * items_per_launch /
@@ -626,6 +723,7 @@ def run_batch_ours(args, cfg):
     achieved = ab[dominant] * S * cfg.num_gates / (kern[dominant] * 1e-3) / 1e9
     traffic = None  # the committed ncu traffic capture is of the C3 20-gate launch
     l1_frac = None
+    clk_mhz = clocks.summary()["sm_mhz"] or clocks.max_mhz or 1965.0
     pair_gbs = ab["pair"] * cfg.batch * cfg.num_gates / (ms_step * 1e-3) / 1e9
 
     # e2e: every step uploads the local slices' sinograms from pinned host memory
@@ -695,13 +793,8 @@ def run_batch_ours(args, cfg):
                                    f"GPU(s)", "mode": "spdhg-batch",
                        "parallelism": f"slice-shard x{world} (no collective)",
                        "l2": "per-epoch working set > 1 GB > 126 MB L2 (no flush needed)"},
-            "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved,
-                         "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                         "traffic": traffic, "peak_source": peak_src,
-                         "bytes_model": "SpMV-equivalent algorithmic bytes, SURVEY.md §8d",
-                         "l1_data_pipe_frac": l1_frac,
-                         "limiter": "L1 data pipe (taps served from L1/L2; ncu LSU wavefronts "
-                                    "vs peak, profiles/ncu_traffic.json)"},
+            "roofline": roofline_line(cfg, kern, S * cfg.num_gates, None, None, clk_mhz,
+                                      hbm_peak, peak_src),
             "roofline_pair": {"achieved_alg_gbs": pair_gbs, "frac_alg": pair_gbs / hbm_peak},
             "kernel_ms_per_epoch_rank0": kern,
             "e2e": e2e,

@@ -244,8 +244,8 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     p->wy = num_bins + 2 * pb;
     size_t off = 0;
     // item region: the prefix every item uses (paired or not) -- A^* partial-image
-    // slots, K2 ray-split partials and arrival counters -- then the single-item
-    // (mirror) layouts: pair-packed float2 (v[i], v[i+1] - v[i]) elements, one load
+    // slots -- then what only single items use: K2 ray-split partials and arrival
+    // counters, and the mirror layouts: pair-packed float2 (v[i], v[i+1] - v[i]) elements, one load
     // fetches both interpolation taps, two per float4 element: the item and its
     // column mirror (X, XT), angles q and A-q (DY rows 1 .. (A-1)/2; row 0 holds the
     // self-paired angles 0 and A/2) -- see mct_internal.cuh
@@ -254,13 +254,13 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     // A^* partial-image slots: the largest angle split any launch of this plan may
     // use (choose_asplit never exceeds it)
     off += p->img_slot_bytes * (size_t)adj_plan_slots(p);
+    p->wsg.pre_bytes = off;  // paired items use only their A^* slots (K2 pairs: no ray split)
     p->off_part = off;
     p->ksplit1 = choose_ksplit(num_angles, num_bins, std::max(rows, cols));
     off += align256((size_t)p->ksplit1 * num_angles * num_bins * sizeof(double));
     p->off_cnt = off;
     off += align256((size_t)((num_angles + MCT_FWD_ANGLES - 1) / MCT_FWD_ANGLES) *
                     ((num_bins + 31) / 32) * sizeof(int));
-    p->wsg.pre_bytes = off;
     p->off_x = off;
     off += align256((size_t)rows * p->wx * sizeof(float4));
     p->off_xt = off;

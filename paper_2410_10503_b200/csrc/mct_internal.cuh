@@ -60,7 +60,7 @@ struct AdjAngle {
 
 struct WsGeom {
     size_t item_bytes;  // a single region
-    size_t pre_bytes;   // IMG slots + K2 partials + counters (prefix of an item region)
+    size_t pre_bytes;   // A^* IMG slots (prefix of an item region)
     size_t pair_bytes;  // interleaved X / XT / DY of a gate pair
     size_t pair_block;  // pair_bytes + 2 * pre_bytes
 };
@@ -81,14 +81,14 @@ struct mct_ray_plan {
 // K2 may split every ray's sample walk into ksplit consecutive parts handled by
 // different blocks (shorter blocks -> better load balance of single-gate SPDHG
 // launches); the last block of a tile to finish sums the fp64 partials in part
-// order and runs the epilogue.  A launch whose slices carry one gate each uses
-// the plan's ksplit1 (enough parts to fill about one wave of resident blocks,
-// clamped to [MCT_KSPLIT_MIN, MCT_KSPLIT_MAX]); several gates per slice use 1.
-// ksplit1 depends only on the plan, so K2 runs the same arithmetic for a batch of
-// slices and a single slice (and for PDHG and a full-draw SPDHG step).  K3's
-// angle split (choose_asplit) follows the launch's tile count instead: a batch
-// and a single slice agree to fp32 rounding, bitwise whenever the splits agree
-// (a plan-constant split costs the 64-slice C5 batch 3.4 %).
+// order and runs the epilogue.  Single items (mirror walks) of a launch whose
+// slices carry one gate each use the plan's ksplit1 (enough parts to fill about one
+// wave of resident blocks, clamped to [MCT_KSPLIT_MIN, MCT_KSPLIT_MAX]); gate pairs
+// and several gates per slice use 1 (their grids already span many waves), so only
+// single regions hold ray-split partials.  A batch of slices therefore agrees with
+// single-slice runs to fp32 rounding (mirror walks, ray split, and K3's angle split
+// choose_asplit, which follows the launch's tile count), bitwise for A^* whenever the
+// splits agree (a plan-constant A^* split costs the 64-slice C5 batch 3.4 %).
 #ifndef MCT_KSPLIT_MIN
 #define MCT_KSPLIT_MIN 2
 #endif
@@ -119,13 +119,14 @@ __host__ __device__ __forceinline__ int mct_half_q(int A) { return 1 + ((A - 1) 
 // Workspace layout (one per launch family; every region keeps one role for every
 // launch size, so pads zeroed once stay zero):
 //   [single region 0 | single region 1 | pair block 0 | pair block 1 | ...]
-// A single region (item_bytes) is the full item layout (IMG slots, K2 partials and
-// arrival counters, then X / XT / DY of the mirror kernels) of an unpaired item:
-// unpaired item k of a launch (k = item - pair_items, at most two: an odd last item
-// and / or a half item) uses single region k.  Pair block p is the interleaved pair
-// region (X / XT / DY of items 2p, 2p+1, pair_bytes) followed by the two items'
-// *prefixes* (pre_bytes: IMG slots, partials, counters) -- paired items never touch
-// the single-item X / XT / DY, so they hold no copy of them.
+// A single region (item_bytes) is the full item layout (A^* IMG slots, then the K2
+// ray-split partials and arrival counters and the X / XT / DY of the mirror
+// kernels) of an unpaired item: unpaired item k of a launch (k = item - pair_items,
+// at most two: an odd last item and / or a half item) uses single region k.  Pair
+// block p is the interleaved pair region (X / XT / DY of items 2p, 2p+1,
+// pair_bytes) followed by the two items' *prefixes* (pre_bytes: the IMG slots) --
+// gate-pair K2 launches never split rays and paired items never touch the
+// single-item X / XT / DY, so a pair block holds no copy of them.
 __host__ __device__ __forceinline__ size_t mct_pair_off(int pair, const WsGeom& g) {
     return 2 * g.item_bytes + (size_t)pair * g.pair_block;
 }

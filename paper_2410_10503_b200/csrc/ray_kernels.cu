@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
     fwd_kernel(FwdArgs p) {
     using V = float4;
     constexpr int G = 2;
-    const int ks = p.ksplit;
+    const int ks = MIR ? p.ksplit : 1;  // gate pairs never split rays (launch_fwd)
     const int group = blockIdx.z / ks;  // item (MIR) or gate pair
     const int part = blockIdx.z - group * ks;
     // LPT (single-gate launches): grid (angle groups, bin tiles by distance rank, parts): every angle group's
@@ -913,6 +913,7 @@ cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st
         FwdArgs a = a_in;
         a.item0 = 0;
         a.n_items = items;
+        a.ksplit = 1;  // >= 2 items fill the GPU without splitting rays (no partials)
         dim3 grid(ntile, (a.A + FWD_ANGLES - 1) / FWD_ANGLES, (np / 2) * a.ksplit);
         if (mode == 0)
             fwd_kernel<0, 0, 0><<<grid, block, 0, s>>>(a);

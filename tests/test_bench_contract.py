@@ -48,8 +48,11 @@ def test_our_arm_json_line(config):
         assert key in line, key
     assert line["value"] > 0 and line["unit"] == "epochs/s" and line["n_gpus"] == 1
     r = line["roofline"]
-    assert r["bound"] == "hbm" and r["achieved"] > 0 and r["peak"] > 0
+    assert r["bound"] == "l1_data_pipe" and r["achieved"] > 0 and r["peak"] > 0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert 0 < r["frac"] <= 1.1  # a physical fraction of the data-pipe peak
+    assert set(r["kernels"]) == {"K2_forward_dual", "K3_adjoint"}
+    assert r["hbm"]["peak"] > 0 and r["hbm"]["compulsory_frac"] < 1.0
     e = line["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert line["gpu_launches"] >= 4 * line["steps"]

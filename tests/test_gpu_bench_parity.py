@@ -86,6 +86,7 @@ def check_state(x, z, y, ost, label):
     ex = strict_rel(x, ost.x)
     ez = strict_rel(z, ost.z)
     ey = stacked_rel(y, ost.y)
+    print(f"PARITY {label}: x {ex:.3e}  z {ez:.3e}  y {ey:.3e}")
     assert ex <= ITER_TOL, f"{label}: x rel L2 {ex:.3e}"
     assert ez <= ITER_TOL, f"{label}: z rel L2 {ez:.3e}"
     assert ey <= ITER_TOL, f"{label}: y rel L2 {ey:.3e}"
@@ -106,8 +107,8 @@ def test_c3_pdhg_5_epochs_bench_path_vs_oracle(m):
     assert np.linalg.norm(ost.x) > 0
     xg, zg, yg = run_capture(m, cfg, problem, graph=True)
     xe, ze, ye = run_capture(m, cfg, problem, graph=False)
-    check_state(xg, zg, yg, ost, "graph")
-    check_state(xe, ze, ye, ost, "eager")
+    check_state(xg, zg, yg, ost, "c3 pdhg graph")
+    check_state(xe, ze, ye, ost, "c3 pdhg eager")
     assert np.array_equal(xg, xe)  # graph replay == eager launches, bit for bit
 
 
@@ -164,6 +165,7 @@ def test_c5_batch_slices_vs_per_slice_oracle(m):
         ost, _ = osolver.run(ocfg, cfgw.alpha, oracle_ops(cfgw, inps[s]), list(probs[s].data),
                              diagnostics=False)
         e = strict_rel(out[s][0], ost.x)
+        print(f"PARITY c5 slice {s}: x {e:.3e}")
         assert e <= ITER_TOL, f"slice {s}: x rel L2 {e:.3e}"
 
 
