@@ -504,3 +504,31 @@ def test_large_batches_match_single_items(m, n, A, B, batch):
         assert rel_l2(fb[i].double().cpu().numpy(), op.apply(x[i]).double().cpu().numpy()) <= 1e-6
         assert rel_l2(ab[i].double().cpu().numpy(),
                       op.adjoint_apply(y[i]).double().cpu().numpy()) <= 1e-6
+
+
+@pytest.mark.parametrize("batch", [16, 17, 20, 33])
+@pytest.mark.parametrize("shape", [(48, 40, 30, 70, 1.0), (33, 64, 31, 80, 0.9),
+                                   (64, 64, 200, 91, 1.0)])
+def test_many_item_batches_match_single_items_and_oracle(m, batch, shape):
+    """PDHG-sized launches (16-33 items: gate pairs, plus the mirror kernels for an
+    odd last item on the side stream): every item agrees with its single-item call
+    and with the fp64 oracle, and the launch is deterministic."""
+    import torch
+
+    geom = m.Geometry(*shape)
+    op = m.RayTransform(geom)
+    orc = oracle.RayTransform(oracle.Geometry(*shape))
+    x = torch.randn(batch, geom.rows, geom.cols, device="cuda")
+    yb = op.forward_batch(x)
+    y = torch.randn(batch, geom.num_angles, geom.num_bins, device="cuda")
+    xb = op.adjoint_batch(y)
+    for i in range(batch):
+        xi = x[i].double().cpu().numpy()
+        yi = y[i].double().cpu().numpy()
+        assert rel_l2(yb[i].double().cpu().numpy(), op.apply(x[i]).double().cpu().numpy()) <= 1e-6
+        assert rel_l2(yb[i].double().cpu().numpy(), orc.apply(xi)) <= TOL, i
+        # A^*: bitwise whenever the angle splits agree, else fp32 rounding
+        assert rel_l2(xb[i].double().cpu().numpy(),
+                      op.adjoint_apply(y[i]).double().cpu().numpy()) <= 1e-6
+        assert rel_l2(xb[i].double().cpu().numpy(), orc.adjoint_apply(yi)) <= TOL, i
+    assert torch.equal(yb, op.forward_batch(x)) and torch.equal(xb, op.adjoint_batch(y))

@@ -555,3 +555,30 @@ def test_step_divergence_leaves_state_at_last_good_iterate(m, golden_tiny):
     # the iterate is still the last finite one: stepping again raises again
     with pytest.raises(m.DivergenceError):
         m.step(st, cfg, problem, lambda: (0, 1, 2, 3))
+
+
+def test_run_batch_17_slices_equal_single_runs(m):
+    """17 slices of one gate per SPDHG iteration: every launch holds 8 slice pairs
+    plus an odd last slice (mirror kernels on the side stream); every slice matches
+    its own run() and the fp64 oracle."""
+    from paper_2410_10503_b200 import workloads
+
+    cfgw = workloads.WorkloadConfig("batch_groups", 40, 36, 61, 3, "dense", 4, 1e-2, 2, peak=2.0)
+    S = 17
+    probs, inps = [], []
+    for s in range(S):
+        p, _, inp = m.simulate.workload_problem(cfgw, s)
+        probs.append(p)
+        inps.append(inp)
+    norms = [1.1 * m.power_method(op, iterations=20) for op in probs[0].operators]
+    cfgs = [m.default_config("spdhg", norms, cfgw.alpha, cfgw.epochs, seed=7 + s)
+            for s in range(S)]
+    out = m.run_batch(cfgs, probs)
+    geom = oracle.Geometry(*cfgw.geometry_args)
+    for s in (0, 5, 15, 16):
+        xs, _ = m.run(cfgs[s], probs[s], diagnostics=False)
+        assert rel_l2(out[s][0], xs) <= 1e-6, s
+        ocfg = osolver.default_config("spdhg", norms, cfgw.alpha, cfgw.epochs, seed=7 + s)
+        st, _ = osolver.run(ocfg, cfgw.alpha, oracle.gate_operators(geom, inps[s].gates),
+                            list(probs[s].data), diagnostics=False)
+        assert np.linalg.norm(st.x) > 0 and rel_l2(out[s][0], st.x) <= ITER_TOL, s
