@@ -201,6 +201,29 @@ def l1_peak_gbs(sm_mhz):
     return 128.0 * sms * float(sm_mhz) * 1e6 / 1e9
 
 
+def pattern_cycles(cfg):
+    """Mean L1 cost (SM cycles per 32-lane 16-byte request) of each gather's access
+    pattern, from the measured cost-vs-lane-spacing curve (tools/micro/l1_pattern.cu,
+    profiles/l1_pattern.json: 4 cycles while 8 consecutive lanes stay inside 128 bytes,
+    i.e. spacing <= 1 element, rising to 8 cycles at spacing >= 1.2), averaged over the
+    geometry's angles (equal weight per angle).  K2: the 32 bins of a warp sit
+    sp/|cos| (rows-dominant) or sp/sin (cols-dominant) elements apart; K3: the 32
+    columns of a warp map to bins |cos|/sp apart."""
+    p = ROOT / "profiles" / "l1_pattern.json"
+    if not p.exists():
+        return None
+    runs = json.loads(p.read_text())["runs"]
+    xs = np.array([r["P"] for r in runs])
+    ys = np.array([r["cycles_per_request"] for r in runs])
+    th = np.arange(cfg.num_angles) * (np.pi / cfg.num_angles)
+    c, s = np.abs(np.cos(th)), np.abs(np.sin(th))
+    sp = 1.0  # BASELINE geometries: unit detector spacing
+    p2 = np.where(c >= s, sp / np.maximum(c, 1e-12), sp / np.maximum(s, 1e-12))
+    p3 = c / sp
+    f = lambda P: float(np.interp(np.minimum(P, xs[-1]), xs, ys).mean())
+    return {"K2_forward_dual": f(p2), "K3_adjoint": f(p3)}
+
+
 def roofline_line(cfg, kern_ms, items, traffic_all, wave_frac, sm_mhz, hbm_peak, peak_src):
     """The bench line's ``roofline``: the limiter that binds K2 / K3 is the L1 data
     pipe (ncu: LSU wavefronts 96 % / 75 % of peak, DRAM < 3 %), so the headline
@@ -211,11 +234,16 @@ def roofline_line(cfg, kern_ms, items, traffic_all, wave_frac, sm_mhz, hbm_peak,
     (gate-slices) one step's launches process."""
     l1b = l1_operand_bytes(cfg)
     peak = l1_peak_gbs(sm_mhz)
+    pat = pattern_cycles(cfg) or {}
     per = {}
     for k in ("K2_forward_dual", "K3_adjoint"):
         gbs = l1b[k] * items / (kern_ms[k] * 1e-3) / 1e9
+        # the access pattern's own ceiling: 512 B per request every `cycles` SM clocks
+        ppk = peak * 4.0 / pat[k] if k in pat else None
         per[k] = {"ms": kern_ms[k], "operand_bytes": l1b[k] * items, "achieved": gbs,
                   "frac": gbs / peak,
+                  "pattern_cycles_per_request": pat.get(k),
+                  "pattern_peak": ppk, "frac_of_pattern_peak": gbs / ppk if ppk else None,
                   "l1_wavefront_frac_ncu": (wave_frac or {}).get(k),
                   "dram_bytes_ncu": (traffic_all or {}).get(k)}
     dominant = max(per, key=lambda k: per[k]["ms"])
