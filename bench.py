@@ -648,6 +648,7 @@ def run_ours(args, cfg):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches_per_step * args.steps,
+            "device_memory": device_memory(torch),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -655,6 +656,13 @@ def run_ours(args, cfg):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def device_memory(torch):
+    """Peak device memory of this process (torch's allocator: the engine's data,
+    duals, state and workspace all live there)."""
+    return {"peak_allocated_bytes": int(torch.cuda.max_memory_allocated()),
+            "peak_reserved_bytes": int(torch.cuda.max_memory_reserved())}
 
 
 def run_batch_ours(args, cfg):

@@ -124,6 +124,7 @@ AdjArgs adj_args(const mct_ray_plan* rp, const void* ws) {
     a.last_part = 0;
     a.asplit = 1;
     a.kfoot = rp->kfoot;
+    a.segw = rp->adj_segw;
     return a;
 }
 
@@ -232,7 +233,10 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
         adj[a].step = (float)(1.0 / m);
         adj[a].g = (float)(spacing / m);
         hmax = std::max(hmax, m / spacing);
+        p->h_acs.push_back(fabs(c) / spacing);
+        p->h_asn.push_back(fabs(s) / spacing);
     }
+    p->adj_segw = adj_segw(p);
     // adjoint footprint: bins within hmax of the pixel's detector coordinate
     // (any positive spacing, projector.py:63-68; K > 3 runs the runtime-K kernel)
     const int K = std::max(0, (int)ceil(hmax - 1e-12) - 1);

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
+#include <vector>
 
 #include "../../include/mctomo_b200.h"
 
@@ -76,6 +77,8 @@ struct mct_ray_plan {
     size_t off_px, off_pxt, off_pdy;  // pair region (see top)
     WsGeom wsg;                       // workspace layout (see mct_item_off)
     int ksplit1;  // K2 ray split of single-gate launches (see MCT_KSPLIT_MIN)
+    std::vector<double> h_acs, h_asn;  // |cos| / sp, |sin| / sp per angle (host)
+    int adj_segw;                      // A^* staged segment length (adj_segw)
 };
 
 // K2 may split every ray's sample walk into ksplit consecutive parts handled by
@@ -254,6 +257,7 @@ struct AdjArgs {
     int n_items, last_part;  // items of the whole call; see ItemSel::last_part
     int asplit;
     int kfoot;               // adjoint footprint (bins thi-kfoot .. thi+kfoot+1)
+    int segw;                // staged sinogram segment length (K = 0, ADJ_TMA)
 };
 
 struct UpdArgs {
@@ -284,6 +288,8 @@ cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, cudaStream_t st);
 int choose_asplit(const mct_ray_plan* rp, int items, int last_part = 0);
 int adj_plan_slots(const mct_ray_plan* rp);
 int choose_ksplit(int A, int B, int n);
+int adj_segw(const mct_ray_plan* rp);
+size_t adj_stage_bytes(int G, int segw);
 cudaError_t launch_update(const UpdArgs& a, int mode, int slices, cudaStream_t st);
 cudaError_t launch_z_update(long long n, const float* dz, float* z, float* zbar, float theta,
                             cudaStream_t st);

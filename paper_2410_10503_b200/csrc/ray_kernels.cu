@@ -10,6 +10,7 @@
 
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <utility>
 
 namespace {
@@ -516,6 +517,53 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
 #define ADJ_SPLIT_RULE 1
 #endif
 #define INV_2_32 2.3283064365386963e-10f
+#ifndef ADJ_TMA
+#define ADJ_TMA 1      // K = 0 gate pairs: sinogram segments staged in shared memory by TMA
+#endif
+#ifndef ADJ_TMA1
+#define ADJ_TMA1 0     // the same for single items (mirror layout): 4 % slower at C3 SPDHG
+#endif
+#define ADJ_STAGED(K, G) ((K) == 0 && ((G) == 2 ? ADJ_TMA : ADJ_TMA1))
+#ifndef ADJ_TC
+#define ADJ_TC 4       // angle pairs per TMA stage
+#endif
+#ifndef ADJ_NST
+#define ADJ_NST 2      // stage buffers (ring): one computed, NST - 1 in flight
+#endif
+#ifndef ADJ_STAGE_FULL
+#define ADJ_STAGE_FULL 1  // guard-free row loop for full tiles in the staged kernel
+#endif
+#ifndef ADJ_SEGW
+#define ADJ_SEGW 40    // staged segment capacity (elements); larger plans take the unstaged path
+#endif
+
+// 1-D TMA (cp.async.bulk) global -> shared with mbarrier completion (sm_90+).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 // One tent (bin index thi, fraction tlo/2^32) applied to two sinogram rows, the
 // row of pixel p at angle a and the row of its mirror at A-a:
@@ -523,27 +571,35 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
 //     (slot 0: angle a, slot 1: angle A-a) -- one 16-byte load;
 //   G = 2 (gate pairs): rows a and a + delta of the pair region, each float4
 //     holding the two items' pairs.
-template <int K, int G>
-__device__ __forceinline__ void adj_tap2(const float4* __restrict__ DY2, unsigned tlo, int thi,
-                                         int delta, float g32, float omg, float* acc_a,
-                                         float* acc_b, int kr) {
+// The K = 0 tent on loaded elements: v = the row of angle a at the bin, vm = the
+// row of angle A-a (G = 2; G = 1: both angles are the two slots of v).
+template <int G>
+__device__ __forceinline__ void adj_fma2(const float4& v, const float4& vm, unsigned tlo,
+                                         float g32, float omg, float* acc_a, float* acc_b) {
     const float F = (float)tlo;
-    if (K == 0 && G == 1) {
-        const float4 v = __ldg(DY2 + (unsigned)thi);
-        const float w0 = __saturatef(fmaf(-F, g32, 1.0f));  // bin floor(jc)
-        const float w1 = __saturatef(fmaf(F, g32, omg));    // bin floor(jc) + 1
+    const float w0 = __saturatef(fmaf(-F, g32, 1.0f));  // bin floor(jc)
+    const float w1 = __saturatef(fmaf(F, g32, omg));    // bin floor(jc) + 1
+    if (G == 1) {
         acc_a[0] = fmaf(w0, v.x, fmaf(w1, v.y, acc_a[0]));
         acc_b[0] = fmaf(w0, v.z, fmaf(w1, v.w, acc_b[0]));
-    } else if (K == 0) {
-        const float4 v = __ldg(DY2 + (unsigned)thi);
-        const float4 vm = __ldg(DY2 + (unsigned)(thi + delta));
-        const float w0 = __saturatef(fmaf(-F, g32, 1.0f));  // bin floor(jc)
-        const float w1 = __saturatef(fmaf(F, g32, omg));    // bin floor(jc) + 1
+    } else {
 #pragma unroll
         for (int h = 0; h < G; ++h) {
             acc_a[h] = fmaf(w0, tv(v, h), fmaf(w1, td(v, h), acc_a[h]));
             acc_b[h] = fmaf(w0, tv(vm, h), fmaf(w1, td(vm, h), acc_b[h]));
         }
+    }
+}
+
+template <int K, int G>
+__device__ __forceinline__ void adj_tap2(const float4* __restrict__ DY2, unsigned tlo, int thi,
+                                         int delta, float g32, float omg, float* acc_a,
+                                         float* acc_b, int kr) {
+    const float F = (float)tlo;
+    if (K == 0) {
+        const float4 v = __ldg(DY2 + (unsigned)thi);
+        const float4 vm = G == 1 ? v : __ldg(DY2 + (unsigned)(thi + delta));
+        adj_fma2<G>(v, vm, tlo, g32, omg, acc_a, acc_b);
     } else {
         const float d = F * INV_2_32;
         const float g = g32 * 4294967296.0f;
@@ -605,7 +661,7 @@ __device__ __forceinline__ void adj_tap1(const float4* __restrict__ DY2, unsigne
                        // batch and a single item agree bitwise)
 #endif
 #ifndef ADJ_MIN_BLOCKS2
-#define ADJ_MIN_BLOCKS2 6
+#define ADJ_MIN_BLOCKS2 5  // staged (TMA) gate-pair kernel: shared memory allows 5 blocks/SM anyway
 #endif
 template <int G> struct AdjShape;
 #ifndef ADJ_TU2
@@ -628,6 +684,12 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
     __shared__ int4 s_u[ADJ_CH];       // sin/sp (lo, hi), g*2^-32, 1 - g
     __shared__ int s_d[ADJ_CH];        // sinogram offset of row A-a relative to row a
     __shared__ double s_tot[G][2 * PPT][ADJ_THREADS];
+    // TMA staging (K = 0): per angle pair the block's sinogram segments -- the bins
+    // under the tile's primary columns and under its mirror columns, in row a (and
+    // row A-a, G = 2) -- first element and length; two stage buffers of ADJ_TC pairs
+    __shared__ int4 s_lo[ADJ_STAGED(K, G) ? ADJ_CH : 1];
+    __shared__ unsigned long long s_full[ADJ_NST];
+    extern __shared__ float4 s_stage[];
     const int group = blockIdx.z / p.asplit;
     const int split = blockIdx.z - group * p.asplit;
     const int A = p.A;
@@ -668,6 +730,15 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
     for (int h = 0; h < G; ++h)
 #pragma unroll
         for (int m = 0; m < 2 * PPT; ++m) s_tot[h][m][tid] = 0.0;
+    constexpr bool STAGED = ADJ_STAGED(K, G);
+    // stage ring: full[b] completes when the bytes of the stage in buffer b landed
+    // (TMA transaction count); `uses` counts the stages run through the ring so far
+    // (buffer = use % NST, parity = (use / NST) & 1)
+    unsigned uses = 0;
+    if (STAGED && tid == 0) {
+        for (int b = 0; b < ADJ_NST; ++b) mbar_init(&s_full[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
 
     // ---- self-paired angles 0 and A/2 (split 0 only), pixel by pixel
     if (split == 0 && singles) {
@@ -713,8 +784,127 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
             s_u[tid] = make_int4((int)(unsigned)aa.snx, (int)(aa.snx >> 32),
                                  __float_as_int(aa.g * INV_2_32), __float_as_int(1.0f - aa.g));
             s_d[tid] = (A - 2 * a) * p.wy;
+            if (STAGED) {
+                // element range of the tile at this angle: T(x, r) = TA + x csx - r snx is
+                // linear, so its integer part is extremal at the corners (x in [0, X1]
+                // primary / mirrored, r in [0, R1])
+                const int X1 = min(ADJ_TW - 1, ncl - 1 - c0);
+                const int R1 = min(TH, p.rows - r0) - 1;
+                const long long xm0 = (long long)(p.cols - 1 - 2 * c0);
+                auto rng = [&](long long x0, long long x1, int& lo, int& n) {
+                    const long long e[4] = {TA + x0 * aa.csx, TA + x1 * aa.csx,
+                                            TA + x0 * aa.csx - R1 * aa.snx,
+                                            TA + x1 * aa.csx - R1 * aa.snx};
+                    int l = (int)(e[0] >> 32), h = l;
+#pragma unroll
+                    for (int k = 1; k < 4; ++k) {
+                        l = min(l, (int)(e[k] >> 32));
+                        h = max(h, (int)(e[k] >> 32));
+                    }
+                    lo = l;
+                    n = min(h - l + 1, ADJ_SEGW);  // the host's bound (launch_adj_g) holds
+                };
+                int lc, nc, lm, nm;
+                rng(0, X1, lc, nc);
+                rng(xm0 - X1, xm0, lm, nm);
+                s_lo[tid] = make_int4(lc, nc, lm, nm);
+            }
         }
         __syncthreads();
+        if constexpr (STAGED) {
+            // stage ring of NST buffers: while the block computes stage s, stages
+            // s + 1 .. s + NST - 1 are in flight; thread 0 refills the buffer of stage s
+            // with stage s + NST once every warp left it (__syncthreads, then an
+            // async-proxy fence before the TMA writes)
+            constexpr int NSEG = G == 2 ? 4 : 2;
+            constexpr int segw = ADJ_SEGW;
+            const int nst = (cnt + ADJ_TC - 1) / ADJ_TC;
+            auto issue = [&](int st) {  // stage st of this chunk (ring use uses + st)
+                const unsigned u = uses + (unsigned)st;
+                const int b = (int)(u % ADJ_NST);
+                fence_proxy_async();
+                const int t0 = st * ADJ_TC, t1 = min(cnt, t0 + ADJ_TC);
+                unsigned bytes = 0;
+                for (int t = t0; t < t1; ++t) {
+                    const int4 L = s_lo[t];
+                    bytes += (unsigned)(L.y + L.w) * 16u * (G == 2 ? 2u : 1u);
+                }
+                mbar_expect_tx(&s_full[b], bytes);
+                for (int t = t0; t < t1; ++t) {
+                    const int4 L = s_lo[t];
+                    float4* dst = s_stage + (size_t)(b * ADJ_TC + (t - t0)) * NSEG * segw;
+                    tma_load_1d(dst, DY2 + L.x, L.y * 16u, &s_full[b]);
+                    tma_load_1d(dst + segw, DY2 + L.z, L.w * 16u, &s_full[b]);
+                    if (G == 2) {
+                        const int dl = s_d[t];
+                        tma_load_1d(dst + 2 * segw, DY2 + L.x + dl, L.y * 16u, &s_full[b]);
+                        tma_load_1d(dst + 3 * segw, DY2 + L.z + dl, L.w * 16u, &s_full[b]);
+                    }
+                }
+            };
+            if (tid == 0)
+                for (int st = 0; st < min(nst, ADJ_NST); ++st) issue(st);
+            float acc[PPT][G], accm[PPT][G];
+#pragma unroll
+            for (int m = 0; m < PPT; ++m)
+#pragma unroll
+                for (int h = 0; h < G; ++h) acc[m][h] = accm[m][h] = 0.0f;
+            for (int st = 0; st < nst; ++st) {
+                const unsigned u = uses + (unsigned)st;
+                const int b = (int)(u % ADJ_NST);
+                mbar_wait(&s_full[b], (u / ADJ_NST) & 1u);
+                const int t0 = st * ADJ_TC, t1 = min(cnt, t0 + ADJ_TC);
+                // FULL: all PPT rows in the image (warp-uniform), no per-row guard
+                auto stage = [&](auto full) {
+                    constexpr bool FULL = decltype(full)::value;
+#pragma unroll 2
+                    for (int t = t0; t < t1; ++t) {
+                        const longlong2 T2 = s_t[t];
+                        const int4 U = s_u[t];
+                        const int4 L = s_lo[t];
+                        const long long snx = ((long long)U.y << 32) | (unsigned)U.x;
+                        const long long snr = RSTEP * snx;
+                        const float g32 = __int_as_float(U.z), omg = __int_as_float(U.w);
+                        const long long T = T2.x + (long long)txc * T2.y - row_off * snx;
+                        const long long Tm = T2.x + (long long)(cmc - c0) * T2.y - row_off * snx;
+                        unsigned tlo = (unsigned)T, thi = (unsigned)(T >> 32);
+                        unsigned mlo = (unsigned)Tm, mhi = (unsigned)(Tm >> 32);
+                        // segments: [primary, row a | mirror, row a | primary, row A-a |
+                        // mirror, row A-a], each segw elements
+                        const float4* sb = s_stage + (size_t)(b * ADJ_TC + (t - t0)) * NSEG * segw;
+#pragma unroll
+                        for (int m = 0; m < PPT; ++m) {
+                            if (FULL || m < nrows) {
+                                const int ic = (int)thi - L.x, im = segw + (int)mhi - L.z;
+                                const float4 v = sb[ic];
+                                const float4 vm = G == 2 ? sb[2 * segw + ic] : v;
+                                adj_fma2<G>(v, vm, tlo, g32, omg, acc[m], accm[m]);
+                                const float4 w = sb[im];
+                                const float4 wm = G == 2 ? sb[2 * segw + im] : w;
+                                adj_fma2<G>(w, wm, mlo, g32, omg, accm[m], acc[m]);
+                            }
+                            fx_sub(tlo, thi, (unsigned)snr, (unsigned)(snr >> 32));
+                            fx_sub(mlo, mhi, (unsigned)snr, (unsigned)(snr >> 32));
+                        }
+                    }
+                };
+                if (ADJ_STAGE_FULL && nrows == PPT)
+                    stage(std::true_type{});
+                else if (nrows > 0)
+                    stage(std::false_type{});
+                __syncthreads();  // every warp is done with buffer b
+                if (tid == 0 && st + ADJ_NST < nst) issue(st + ADJ_NST);
+            }
+            uses += (unsigned)nst;
+#pragma unroll
+            for (int m = 0; m < PPT; ++m)
+#pragma unroll
+                for (int h = 0; h < G; ++h) {
+                    s_tot[h][m][tid] += (double)acc[m][h];
+                    s_tot[h][PPT + m][tid] += (double)accm[m][h];
+                }
+            continue;
+        }
         if (nrows <= 0) continue;
         float acc[PPT][G], accm[PPT][G];
 #pragma unroll
@@ -986,19 +1176,58 @@ static int adj_split_for(long long tiles, long long slots, const mct_ray_plan* r
 #endif
 }
 
-static long long adj_slots(int G) {
-    static long long slots[3] = {0, 0, 0};  // resident adj blocks per GPU (queried once)
-    if (slots[G] == 0) {
-        int dev = 0, sms = 148, per_sm = 8;
-        if (cudaGetDevice(&dev) == cudaSuccess)
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const cudaError_t e =
-            G == 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_kernel<0, 1>, ADJ_THREADS, 0)
-                   : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_kernel<0, 2>, ADJ_THREADS, 0);
-        if (e != cudaSuccess || per_sm < 1) per_sm = 8;
-        slots[G] = (long long)sms * per_sm;
-    }
-    return slots[G];
+// Elements of one staged sinogram segment (see adj_kernel): the bins a tile's
+// primary (or mirror) columns and rows reach at one angle, bounded over the plan's
+// angles from the same fixed-point steps the kernel walks (+ 2 for the floors).
+int adj_segw(const mct_ray_plan* rp) {
+    constexpr int TH = ADJ_PPT * ADJ_WARPS;
+    static_assert(ADJ_PPT == ADJ_PPT2, "one tile height for both A^* kernels");
+    double w = 0.0;
+    for (size_t a = 0; a < rp->h_acs.size(); ++a)
+        w = std::max(w, (ADJ_TW - 1) * rp->h_acs[a] + (TH - 1) * rp->h_asn[a]);
+    return (int)ceil(w) + 3;
+}
+
+// Dynamic shared memory of the staged K = 0 kernel; 0 when the plan's segments do
+// not fit ADJ_SEGW (launch_adj_g then runs the unstaged runtime-footprint kernel).
+size_t adj_stage_bytes(int G, int segw) {
+    return ADJ_STAGED(0, G) && segw <= ADJ_SEGW
+               ? (size_t)ADJ_NST * ADJ_TC * (G == 2 ? 4 : 2) * ADJ_SEGW * sizeof(float4)
+               : 0;
+}
+
+static void adj_configure(int G, size_t dyn) {
+    static std::mutex mu;
+    static size_t done[3] = {0, 0, 0};
+    std::lock_guard<std::mutex> lock(mu);
+    if (done[G] >= dyn + 1) return;
+    done[G] = dyn + 1;
+    const void* f = G == 1 ? (const void*)adj_kernel<0, 1> : (const void*)adj_kernel<0, 2>;
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (ADJ_STAGED(0, G)) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+
+static long long adj_slots(int G, size_t dyn) {
+    // resident adj blocks per GPU, per (G, dynamic shared memory) (queried once)
+    static std::mutex mu;
+    static std::map<std::pair<int, size_t>, long long> slots;
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_pair(G, dyn);
+    auto it = slots.find(key);
+    if (it != slots.end()) return it->second;
+    int dev = 0, sms = 148, per_sm = 8;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const cudaError_t e =
+        G == 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_kernel<0, 1>, ADJ_THREADS, dyn)
+               : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_kernel<0, 2>, ADJ_THREADS, dyn);
+    if (e != cudaSuccess || per_sm < 1) per_sm = 8;
+    return slots[key] = (long long)sms * per_sm;
+}
+static long long adj_slots(int G, const mct_ray_plan* rp) {
+    const size_t dyn = rp->kfoot == 0 ? adj_stage_bytes(G, rp->adj_segw) : 0;
+    adj_configure(G, dyn);
+    return adj_slots(G, dyn);
 }
 
 // A^* partial-image slots a plan's items hold: the single-item split, and at
@@ -1010,7 +1239,7 @@ static long long adj_slots(int G) {
 int adj_plan_slots(const mct_ray_plan* rp) {
     constexpr int TH1 = AdjShape<1>::PPT * ADJ_WARPS;
     const long long tiles1 = (long long)adj_tiles_x(rp->cols) * ((rp->rows + TH1 - 1) / TH1);
-    const int s1 = adj_split_for(tiles1, adj_slots(1), rp);
+    const int s1 = adj_split_for(tiles1, adj_slots(1, rp), rp);
     const long long by_angles =
         rp->A / (2 * MCT_ASPLIT_MIN_PAIRS) > 0 ? rp->A / (2 * MCT_ASPLIT_MIN_PAIRS) : 1;
     const int lo = (int)(by_angles < MCT_MIN_ASLOTS ? by_angles : MCT_MIN_ASLOTS);
@@ -1021,9 +1250,9 @@ int choose_asplit(const mct_ray_plan* rp, int items, int last_part) {
     const int n = items > 0 ? items : 1;
     constexpr int TH1 = AdjShape<1>::PPT * ADJ_WARPS, TH2 = AdjShape<2>::PPT * ADJ_WARPS;
     const long long tiles1 = (long long)adj_tiles_x(rp->cols) * ((rp->rows + TH1 - 1) / TH1);
-    const int s1 = adj_split_for(tiles1, adj_slots(1), rp);  // single item: the plan's slot count
+    const int s1 = adj_split_for(tiles1, adj_slots(1, rp), rp);  // single item: the plan's slot count
     const int np = mct_pair_items(n, last_part);
-    if (np == 0) return n == 1 ? s1 : adj_split_for(tiles1 * n, adj_slots(1), rp);
+    if (np == 0) return n == 1 ? s1 : adj_split_for(tiles1 * n, adj_slots(1, rp), rp);
     // pair launch + (odd last item) single launch run one after the other: the split
     // minimising the sum of their (waves, rounded up) x (angle pairs per block),
     // e.g. C3 with 3 local gates (one rank of 8): 3 splits, each launch one full
@@ -1031,13 +1260,16 @@ int choose_asplit(const mct_ray_plan* rp, int items, int last_part) {
     // waves.  At most the plan's slot count.
     const long long tiles2 = (long long)adj_tiles_x(rp->cols) * ((rp->rows + TH2 - 1) / TH2);
     const long long b2 = tiles2 * (np / 2), b1 = tiles1 * (n - np);
-    const long long sl2 = adj_slots(2), sl1 = adj_slots(1);
+    const long long sl2 = adj_slots(2, rp), sl1 = adj_slots(1, rp);
     const long long P = rp->A > 2 ? (rp->A - 1) / 2 : 1;
     const long long by_angles =
         rp->A / (2 * MCT_ASPLIT_MIN_PAIRS) > 0 ? rp->A / (2 * MCT_ASPLIT_MIN_PAIRS) : 1;
     long long smax = by_angles < MCT_MAX_ASPLIT ? by_angles : MCT_MAX_ASPLIT;
     const long long cap = adj_plan_slots(rp);
     smax = smax < cap ? smax : cap;
+#ifdef MCT_PAIR_ASPLIT_MAX
+    smax = smax < MCT_PAIR_ASPLIT_MAX ? smax : MCT_PAIR_ASPLIT_MAX;
+#endif
     long long best = 1, best_cost = -1;
     for (long long sp = 1; sp <= smax; ++sp) {
         const long long waves = (b2 * sp + sl2 - 1) / sl2 + (b1 * sp + sl1 - 1) / sl1;
@@ -1052,11 +1284,15 @@ int choose_asplit(const mct_ray_plan* rp, int items, int last_part) {
 
 template <int G>
 static void launch_adj_g(const AdjArgs& a, int kfoot, int groups, cudaStream_t st) {
+    // kfoot: by value, may switch to the runtime-footprint kernel below
     constexpr int TH = AdjShape<G>::PPT * ADJ_WARPS;
     dim3 block(ADJ_TW, ADJ_WARPS),
         grid(adj_tiles_x(a.cols), (a.rows + TH - 1) / TH, groups * a.asplit);
+    const size_t dyn = kfoot == 0 ? adj_stage_bytes(G, a.segw) : 0;
+    if (kfoot == 0 && ADJ_STAGED(0, G) && dyn == 0) kfoot = -1;  // segments too long to stage
+    if (kfoot == 0) adj_configure(G, dyn);
     switch (kfoot) {
-        case 0: adj_kernel<0, G><<<grid, block, 0, st>>>(a); break;
+        case 0: adj_kernel<0, G><<<grid, block, dyn, st>>>(a); break;
         case 1: adj_kernel<1, G><<<grid, block, 0, st>>>(a); break;
         case 2: adj_kernel<2, G><<<grid, block, 0, st>>>(a); break;
         case 3: adj_kernel<3, G><<<grid, block, 0, st>>>(a); break;
