@@ -147,13 +147,13 @@ __global__ void pad_sino_kernel(const float* __restrict__ sino, const AdjAngle* 
     float* DY = reinterpret_cast<float*>(
                     ws + (paired ? mct_pair_off(item >> 1, wsg)
                                  : mct_item_off(item, pair_items, wsg)) +
-                    (paired ? off_dy2 : off_dy1)) + 2 * slot;
+                    (paired ? off_dy2 : off_dy1)) + slot;
     const float* s = sino + ((long long)item * A + a) * B;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x) {
         const long long e = 4 * ((long long)row * wy + pb + j);
         const float v = s[j] * step;
-        DY[e] = v;
-        DY[e - 3] = v;
+        DY[e] = v;      // element j: (slot 0, slot 1) at bin j, then at bin j + 1
+        DY[e - 2] = v;  // element j - 1, bin j
     }
 }
 
@@ -198,6 +198,10 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
 // (value, forward difference) of float2 slot h of a float4 element
 __device__ __forceinline__ float tv(const float4& v, int h) { return h ? v.z : v.x; }
 __device__ __forceinline__ float td(const float4& v, int h) { return h ? v.w : v.y; }
+// DY (sinogram increments for A^*) element j: (slot 0, slot 1) at bin j in .xy and
+// at bin j + 1 in .zw, so both slots' taps are float2 lanes (FFMA2 in K3)
+__device__ __forceinline__ float dlo(const float4& v, int h) { return h ? v.y : v.x; }
+__device__ __forceinline__ float dhi(const float4& v, int h) { return h ? v.w : v.z; }
 
 // K2 walks two rays per warp lane at once, one 16-byte load per sample:
 //   MIR = 0 (gate pairs): items 2p, 2p+1 at angle a (pair region);
@@ -463,11 +467,11 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
                 slot = sl < nsingle ? sl : h;
             }
             float* DY = reinterpret_cast<float*>(const_cast<char*>(tb) +
-                                                 (MIR ? p.off_dy : p.off_pdy)) + 2 * slot;
+                                                 (MIR ? p.off_dy : p.off_pdy)) + slot;
             const long long e = 4 * ((long long)row * p.wy + p.pb + j);
             const float dlt = (yn - yv) * ra.step;  // pre-scaled for A^* (see K3)
-            DY[e] = dlt;
-            DY[e - 3] = dlt;
+            DY[e] = dlt;      // element j (bin j of both slots, then bin j + 1)
+            DY[e - 2] = dlt;  // element j - 1, bin j
             if (p.proj) p.proj[off] = proj;
             if (!isfinite(yn) && p.status)
                 atomicMin(p.status + 1, ((unsigned long long)iter << 20) | (unsigned long long)gate);
@@ -533,6 +537,9 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
 #ifndef ADJ_STAGE_FULL
 #define ADJ_STAGE_FULL 1  // guard-free row loop for full tiles in the staged kernel
 #endif
+#ifndef ADJ_FFMA2_1
+#define ADJ_FFMA2_1 1  // single-item A^*: both angles of an element as one FFMA2
+#endif
 #ifndef ADJ_SEGW
 #define ADJ_SEGW 40    // staged segment capacity (elements); larger plans take the unstaged path
 #endif
@@ -579,15 +586,26 @@ __device__ __forceinline__ void adj_fma2(const float4& v, const float4& vm, unsi
     const float F = (float)tlo;
     const float w0 = __saturatef(fmaf(-F, g32, 1.0f));  // bin floor(jc)
     const float w1 = __saturatef(fmaf(F, g32, omg));    // bin floor(jc) + 1
-    if (G == 1) {
-        acc_a[0] = fmaf(w0, v.x, fmaf(w1, v.y, acc_a[0]));
-        acc_b[0] = fmaf(w0, v.z, fmaf(w1, v.w, acc_b[0]));
+    if (G == 1) {  // the element's two slots are angles a (-> acc_a) and A-a (-> acc_b)
+#if ADJ_FFMA2_1
+        float2 a = make_float2(acc_a[0], acc_b[0]);
+        a = __ffma2_rn(make_float2(w0, w0), make_float2(v.x, v.y),
+                       __ffma2_rn(make_float2(w1, w1), make_float2(v.z, v.w), a));
+        acc_a[0] = a.x;
+        acc_b[0] = a.y;
+#else
+        acc_a[0] = fmaf(w0, v.x, fmaf(w1, v.z, acc_a[0]));
+        acc_b[0] = fmaf(w0, v.y, fmaf(w1, v.w, acc_b[0]));
+#endif
     } else {
-#pragma unroll
-        for (int h = 0; h < G; ++h) {
-            acc_a[h] = fmaf(w0, tv(v, h), fmaf(w1, td(v, h), acc_a[h]));
-            acc_b[h] = fmaf(w0, tv(vm, h), fmaf(w1, td(vm, h), acc_b[h]));
-        }
+        // both items at once: per lane the same fmaf(w0, y_j, fmaf(w1, y_j+1, acc))
+        float2 a = make_float2(acc_a[0], acc_a[1]), b = make_float2(acc_b[0], acc_b[1]);
+        a = __ffma2_rn(make_float2(w0, w0), make_float2(v.x, v.y),
+                       __ffma2_rn(make_float2(w1, w1), make_float2(v.z, v.w), a));
+        b = __ffma2_rn(make_float2(w0, w0), make_float2(vm.x, vm.y),
+                       __ffma2_rn(make_float2(w1, w1), make_float2(vm.z, vm.w), b));
+        acc_a[0] = a.x; acc_a[1] = a.y;
+        acc_b[0] = b.x; acc_b[1] = b.y;
     }
 }
 
@@ -609,15 +627,15 @@ __device__ __forceinline__ void adj_tap2(const float4* __restrict__ DY2, unsigne
             const float wb = __saturatef(fmaf(-fabsf((float)(mm + 1) - d), g, 1.0f));
             if (G == 1) {
                 const float4 v = __ldg(DY2 + (thi + mm));
-                acc_a[0] = fmaf(wa, v.x, fmaf(wb, v.y, acc_a[0]));
-                acc_b[0] = fmaf(wa, v.z, fmaf(wb, v.w, acc_b[0]));
+                acc_a[0] = fmaf(wa, v.x, fmaf(wb, v.z, acc_a[0]));
+                acc_b[0] = fmaf(wa, v.y, fmaf(wb, v.w, acc_b[0]));
             } else {
                 const float4 v = __ldg(DY2 + (thi + mm));
                 const float4 vm = __ldg(DY2 + (thi + delta + mm));
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
-                    acc_a[h] = fmaf(wa, tv(v, h), fmaf(wb, td(v, h), acc_a[h]));
-                    acc_b[h] = fmaf(wa, tv(vm, h), fmaf(wb, td(vm, h), acc_b[h]));
+                    acc_a[h] = fmaf(wa, dlo(v, h), fmaf(wb, dhi(v, h), acc_a[h]));
+                    acc_b[h] = fmaf(wa, dlo(vm, h), fmaf(wb, dhi(vm, h), acc_b[h]));
                 }
             }
         }
@@ -635,10 +653,10 @@ __device__ __forceinline__ void adj_tap1(const float4* __restrict__ DY2, unsigne
         const float w0 = __saturatef(fmaf(-F, g32, 1.0f));
         const float w1 = __saturatef(fmaf(F, g32, omg));
         if (G == 1)
-            acc[0] = fmaf(w0, tv(v, slot), fmaf(w1, td(v, slot), acc[0]));
+            acc[0] = fmaf(w0, dlo(v, slot), fmaf(w1, dhi(v, slot), acc[0]));
         else
 #pragma unroll
-            for (int h = 0; h < G; ++h) acc[h] = fmaf(w0, tv(v, h), fmaf(w1, td(v, h), acc[h]));
+            for (int h = 0; h < G; ++h) acc[h] = fmaf(w0, dlo(v, h), fmaf(w1, dhi(v, h), acc[h]));
     } else {
         const float d = F * INV_2_32;
         const float g = g32 * 4294967296.0f;
@@ -648,10 +666,10 @@ __device__ __forceinline__ void adj_tap1(const float4* __restrict__ DY2, unsigne
             const float wa = __saturatef(fmaf(-fabsf((float)mm - d), g, 1.0f));
             const float wb = __saturatef(fmaf(-fabsf((float)(mm + 1) - d), g, 1.0f));
             if (G == 1)
-                acc[0] = fmaf(wa, tv(v, slot), fmaf(wb, td(v, slot), acc[0]));
+                acc[0] = fmaf(wa, dlo(v, slot), fmaf(wb, dhi(v, slot), acc[0]));
             else
 #pragma unroll
-                for (int h = 0; h < G; ++h) acc[h] = fmaf(wa, tv(v, h), fmaf(wb, td(v, h), acc[h]));
+                for (int h = 0; h < G; ++h) acc[h] = fmaf(wa, dlo(v, h), fmaf(wb, dhi(v, h), acc[h]));
         }
     }
 }
