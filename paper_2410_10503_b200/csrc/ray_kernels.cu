@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
 #define ADJ_TMA 1      // K = 0 gate pairs: sinogram segments staged in shared memory by TMA
 #endif
 #ifndef ADJ_TMA1
-#define ADJ_TMA1 0     // the same for single items (mirror layout): 4 % slower at C3 SPDHG
+#define ADJ_TMA1 1     // the same for single items (mirror layout)
 #endif
 #define ADJ_STAGED(K, G) ((K) == 0 && ((G) == 2 ? ADJ_TMA : ADJ_TMA1))
 #ifndef ADJ_TC
