@@ -13,6 +13,9 @@ namespace {
 #ifndef K4_LANES
 #define K4_LANES 4
 #endif
+#ifndef K4_BLOCK1
+#define K4_BLOCK1 256  // threads per block of single-lane (single-gate) launches
+#endif
 #ifndef K4_MINB1
 #define K4_MINB1 0  // single-lane (single-gate) launches: compiler default
 #endif
@@ -33,7 +36,7 @@ namespace {
 // sums in lane order (fixed association: deterministic), so the per-pixel gate
 // chains run LANES-wide in parallel instead of one after the other.
 template <int MODE, int LANES>
-__global__ void __launch_bounds__(LANES > 1 ? 32 * LANES : 256, LANES > 1 ? K4_MINB : K4_MINB1)
+__global__ void __launch_bounds__(LANES > 1 ? 32 * LANES : K4_BLOCK1, LANES > 1 ? K4_MINB : K4_MINB1)
 update_kernel(UpdArgs p) {
     const int slice = blockIdx.y;
     const long long n = (long long)p.rows * p.cols;
@@ -315,7 +318,7 @@ cudaError_t launch_update(const UpdArgs& a, int mode, int slices, cudaStream_t s
         }
         return cudaGetLastError();
     }
-    dim3 block(256), grid((unsigned)((n + 255) / 256), slices);
+    dim3 block(K4_BLOCK1), grid((unsigned)((n + K4_BLOCK1 - 1) / K4_BLOCK1), slices);
     switch (mode) {
         case 0: update_kernel<0, 1><<<grid, block, 0, st>>>(a); break;
         case 1: update_kernel<1, 1><<<grid, block, 0, st>>>(a); break;
