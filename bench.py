@@ -201,14 +201,17 @@ def l1_peak_gbs(sm_mhz):
     return 128.0 * sms * float(sm_mhz) * 1e6 / 1e9
 
 
+FWD_IL = 2  # K2 lane interleave (paper_2410_10503_b200/csrc/mct_internal.cuh MCT_FWD_IL)
+
+
 def pattern_cycles(cfg):
     """Mean L1 cost (SM cycles per 32-lane 16-byte request) of each gather's access
     pattern, from the measured cost-vs-lane-spacing curve (tools/micro/l1_pattern.cu,
     profiles/l1_pattern.json: 4 cycles while 8 consecutive lanes stay inside 128 bytes,
     i.e. spacing <= 1 element, rising to 8 cycles at spacing >= 1.2), averaged over the
-    geometry's angles (equal weight per angle).  K2: the 32 bins of a warp sit
-    sp/|cos| (rows-dominant) or sp/sin (cols-dominant) elements apart; K3: the 32
-    columns of a warp map to bins |cos|/sp apart."""
+    geometry's angles (equal weight per angle).  K2: consecutive bins sit sp/|cos|
+    (rows-dominant) or sp/sin (cols-dominant) elements apart, FWD_IL lanes per bin;
+    K3: the 32 columns of a warp map to bins |cos|/sp apart."""
     p = ROOT / "profiles" / "l1_pattern.json"
     if not p.exists():
         return None
@@ -219,6 +222,10 @@ def pattern_cycles(cfg):
     c, s = np.abs(np.cos(th)), np.abs(np.sin(th))
     sp = 1.0  # BASELINE geometries: unit detector spacing
     p2 = np.where(c >= s, sp / np.maximum(c, 1e-12), sp / np.maximum(s, 1e-12))
+    # K2 lanes interleave FWD_IL nearly parallel rays per bin (csrc MCT_FWD_IL): 8 lanes
+    # span (8 / IL - 1) bin spacings, i.e. the microbenchmark's 8 lanes at spacing
+    # (8 / IL - 1) * P / 7
+    p2 = p2 * (8 / FWD_IL - 1) / 7
     p3 = c / sp
     f = lambda P: float(np.interp(np.minimum(P, xs[-1]), xs, ys).mean())
     return {"K2_forward_dual": f(p2), "K3_adjoint": f(p3)}

@@ -263,21 +263,24 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     p->ksplit1 = choose_ksplit(num_angles, num_bins, std::max(rows, cols));
     off += align256((size_t)p->ksplit1 * num_angles * num_bins * sizeof(double));
     p->off_cnt = off;
-    off += align256((size_t)((num_angles + MCT_FWD_ANGLES - 1) / MCT_FWD_ANGLES) *
-                    ((num_bins + 31) / 32) * sizeof(int));
+    off += align256((size_t)mct_fwd_groups(num_angles) * mct_fwd_btiles(num_bins) * sizeof(int));
+    // X and XT get max(rows, cols) rows: a K2 warp may walk a rows-dominant and a
+    // cols-dominant ray together (MCT_FWD_IL), stepping up to max(rows, cols) rows;
+    // the extra rows stay zero, so the short ray reads zeros there
+    const size_t nrow = (size_t)std::max(rows, cols);
     p->off_x = off;
-    off += align256((size_t)rows * p->wx * sizeof(float4));
+    off += align256(nrow * p->wx * sizeof(float4));
     p->off_xt = off;
-    off += align256((size_t)cols * p->wxt * sizeof(float4));
+    off += align256(nrow * p->wxt * sizeof(float4));
     p->off_dy = off;
     off += align256((size_t)(num_angles / 2 + 1) * p->wy * sizeof(float4));
     p->wsg.item_bytes = off;
     // gate-pair region (interleaved float4 layouts, see mct_internal.cuh)
     size_t poff = 0;
     p->off_px = poff;
-    poff += align256((size_t)rows * p->wx * sizeof(float4));
+    poff += align256(nrow * p->wx * sizeof(float4));
     p->off_pxt = poff;
-    poff += align256((size_t)cols * p->wxt * sizeof(float4));
+    poff += align256(nrow * p->wxt * sizeof(float4));
     p->off_pdy = poff;
     poff += align256((size_t)num_angles * p->wy * sizeof(float4));
     p->wsg.pair_bytes = poff;

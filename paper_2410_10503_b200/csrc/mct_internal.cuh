@@ -101,6 +101,19 @@ struct mct_ray_plan {
 #ifndef MCT_FWD_ANGLES
 #define MCT_FWD_ANGLES 4
 #endif
+// K2 lane interleave: a warp walks 32 / IL bins of IL consecutive angle slots, lane
+// l -> (bin l / IL, slot l % IL), so 8 consecutive lanes span 8 / IL bins x IL nearly
+// parallel rays (see fwd_kernel); a block is MCT_FWD_ANGLES warps.
+#ifndef MCT_FWD_IL
+#define MCT_FWD_IL 2
+#endif
+// K2 tiles of a geometry: angle-slot groups x bin tiles (grid and arrival counters)
+__host__ __device__ __forceinline__ int mct_fwd_groups(int slots) {
+    return (slots + MCT_FWD_ANGLES * MCT_FWD_IL - 1) / (MCT_FWD_ANGLES * MCT_FWD_IL);
+}
+__host__ __device__ __forceinline__ int mct_fwd_btiles(int bins) {
+    return (bins + 32 / MCT_FWD_IL - 1) / (32 / MCT_FWD_IL);
+}
 
 // Items [0, mct_pair_items(n)) of a launch of n items run the gate-pair kernels
 // (consecutive pairs); an odd last item runs the single-item kernels on its own

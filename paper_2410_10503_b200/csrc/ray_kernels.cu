@@ -233,9 +233,15 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
         const int r = jr - 2 * pairs;
         return below > above ? c - 1 - pairs - r : c + 1 + pairs + r;
     }() : (int)blockIdx.x;
-    const int s_raw = (LPT ? blockIdx.x : blockIdx.y) * FWD_ANGLES + threadIdx.y;
+    // lane -> (bin, slot): IL consecutive lanes walk the same bin of IL consecutive angle
+    // slots (nearly parallel rays), so 8 lanes of a request span 8 / IL bins: the L1
+    // delivers a 16-byte request in 4 clocks while 8 consecutive lanes stay inside 128
+    // bytes, 8 clocks once they spread further (tools/micro/l1_pattern.cu)
+    constexpr int IL = MCT_FWD_IL, BW = 32 / IL;
+    const int s_raw = ((LPT ? blockIdx.x : blockIdx.y) * FWD_ANGLES + threadIdx.y) * IL +
+                      (int)threadIdx.x % IL;
     const int nslot = MIR ? mir_slots(p.A) : p.A;
-    bool warp_on = s_raw < nslot;            // warp-uniform; no early exit (block syncs below)
+    bool warp_on = s_raw < nslot;            // per lane; no early exit (block syncs below)
     if (MIR && p.sel.last_part && p.item0 + (int)blockIdx.z / ks == p.n_items - 1) {
         // a half item: slots of the first (part 1) or second (part 2) half of the angle pairs
         const int s_mid = mir_nsingle(p.A) + mct_half_q(p.A) - 1;
@@ -246,7 +252,7 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
     // angle walked by this warp (slot 0); MIR: slot 1 is angle A - a
     const int a = !MIR ? sl : (sl < nsingle ? (sl == 0 ? 0 : p.A / 2) : sl - nsingle + 1);
     const bool pair1 = !MIR || sl >= nsingle;  // slot 1 holds a real ray
-    const int j = btile * 32 + threadIdx.x;
+    const int j = btile * BW + (int)threadIdx.x / IL;
     const bool active = warp_on && j < p.B;
     const int jj = active ? j : p.B - 1;  // idle lanes shadow the last bin (no store)
     const RayAngle ra = p.ang[a];
@@ -305,6 +311,10 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
         float ea[G];  // ragged-edge samples (predicated on the tap range)
 #pragma unroll
         for (int h = 0; h < G; ++h) { dacc[h] = 0.0; ea[h] = 0.0f; }
+        // lanes of one warp may walk different angles (MCT_FWD_IL); with a non-square
+        // image their dominant axes differ in length and the union walk steps past the
+        // shorter one's last row: X / XT carry max(rows, cols) rows, zero beyond the
+        // image, so those samples read zeros
         int k = wlo;
         for (; k < clo; ++k) {
             const int i0 = (int)fhi - rowoff;
@@ -1029,7 +1039,7 @@ int choose_ksplit(int A, int B, int n) {
         slots = sms * per_sm;
     }
     const long long blocks =
-        (long long)((B + 31) / 32) * ((mir_slots(A) + FWD_ANGLES - 1) / FWD_ANGLES);
+        (long long)mct_fwd_btiles(B) * mct_fwd_groups(mir_slots(A));
     long long k = (slots + blocks - 1) / blocks;
     const long long by_len = n / 16 > 1 ? n / 16 : 1;  // >= 16 samples per part
     k = k < by_len ? k : by_len;
@@ -1114,7 +1124,7 @@ static cudaError_t fork_join(cudaStream_t st, MainF main_launch, SideF side_laun
 cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st) {
     fwd_prefer_l1();
     const dim3 block(32, FWD_ANGLES);
-    const unsigned ntile = (a_in.B + 31) / 32;
+    const unsigned ntile = mct_fwd_btiles(a_in.B);
     const int np = mct_pair_items(items, a_in.sel.last_part);
     // gate pairs (bins fastest: L2 locality across pairs)
     auto pairs = [&](cudaStream_t s) {
@@ -1122,7 +1132,7 @@ cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st
         a.item0 = 0;
         a.n_items = items;
         a.ksplit = 1;  // >= 2 items fill the GPU without splitting rays (no partials)
-        dim3 grid(ntile, (a.A + FWD_ANGLES - 1) / FWD_ANGLES, (np / 2) * a.ksplit);
+        dim3 grid(ntile, mct_fwd_groups(a.A), (np / 2) * a.ksplit);
         if (mode == 0)
             fwd_kernel<0, 0, 0><<<grid, block, 0, s>>>(a);
         else
@@ -1137,7 +1147,7 @@ cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st
         a.item0 = np;
         a.n_items = items;
         const int rest = items - np;
-        const unsigned ngroup = (mir_slots(a.A) + FWD_ANGLES - 1) / FWD_ANGLES;
+        const unsigned ngroup = mct_fwd_groups(mir_slots(a.A));
         const bool lpt = a.ksplit > 1 && rest == 1;
         dim3 grid(lpt ? ngroup : ntile, lpt ? ntile : ngroup, rest * a.ksplit);
         if (lpt) {
