@@ -93,7 +93,7 @@ struct mct_ray_plan {
 // choose_asplit, which follows the launch's tile count), bitwise for A^* whenever the
 // splits agree (a plan-constant A^* split costs the 64-slice C5 batch 3.4 %).
 #ifndef MCT_KSPLIT_MIN
-#define MCT_KSPLIT_MIN 2
+#define MCT_KSPLIT_MIN 1
 #endif
 #ifndef MCT_KSPLIT_MAX
 #define MCT_KSPLIT_MAX 4

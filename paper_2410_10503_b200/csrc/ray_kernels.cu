@@ -191,6 +191,9 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
 #ifndef FWD_MIN_BLOCKS2
 #define FWD_MIN_BLOCKS2 8         // gate pairs: 8 x 4 warps resident, 64 registers
 #endif
+#ifndef FWD_LPT_NOSPLIT
+#define FWD_LPT_NOSPLIT 0  // 1: longest-rays-first order for unsplit single-gate walks too
+#endif
 #ifndef FWD_MIN_BLOCKS_M
 #define FWD_MIN_BLOCKS_M 7        // single-item mirror walks (72 registers, no spills)
 #endif
@@ -1148,7 +1151,7 @@ cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st
         a.n_items = items;
         const int rest = items - np;
         const unsigned ngroup = mct_fwd_groups(mir_slots(a.A));
-        const bool lpt = a.ksplit > 1 && rest == 1;
+        const bool lpt = (a.ksplit > 1 || FWD_LPT_NOSPLIT) && rest == 1;
         dim3 grid(lpt ? ngroup : ntile, lpt ? ntile : ngroup, rest * a.ksplit);
         if (lpt) {
             if (mode == 0)
