@@ -402,7 +402,7 @@ def run_ours(args, cfg):
     import paper_2410_10503_b200 as m
     from paper_2410_10503_b200 import _lib
     from paper_2410_10503_b200.distributed import ShardedPDHG
-    from paper_2410_10503_b200.engine import Engine
+    from paper_2410_10503_b200.engine import Engine, KernelTimer
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -457,39 +457,25 @@ def run_ours(args, cfg):
     eng.set_params(pcfg)
     eng.reset()
     items = eng.items_pdhg(epoch_ctr=True)
-    ip, sp = ctypes.byref(items), ctypes.byref(eng._st)
-    fam, ws, st = eng.family.handle, _lib.ptr(eng.ws), _lib.stream_handle(stream)
     names = ["K1_prox_warp", "K2_forward_dual", "K3_adjoint", "K4_adjoint_update"]
-    dz_now = [None]
+    chunks = eng.chunks(eng.local * eng.S, items.last_part)
 
-    def k4():
-        dz_now[0] = worker.partial_buffer() if use_dist else None
-        _lib.check(L.mct_iter_adjoint_update(fam, ip, sp, _lib.ptr(dz_now[0]) if use_dist
-                                             else None, ws, st))
-
-    calls = [
-        lambda: _lib.check(L.mct_iter_prox_warp(fam, ip, sp, eng.tau, problem.alpha, ws, st)),
-        lambda: _lib.check(L.mct_iter_forward_dual(fam, ip, sp, ws, st)),
-        lambda: _lib.check(L.mct_iter_adjoint(fam, ip, ws, st)),
-        k4,
-    ]
-
-    def step_fn(evs=None):
-        for i, call in enumerate(calls):
-            if evs is not None:
-                evs[i].record(stream)
-            call()
-        if evs is not None:
-            evs[4].record(stream)
+    def step_fn(timer=None):
+        # K1 -> K2 -> K3 per chunk of the workspace's pair ring (one chunk up to ~256 MB
+        # of pair regions: C3 runs unchunked), then K4 over every item
+        dz = worker.partial_buffer() if use_dist else None
+        eng.iteration(items, problem.alpha, dz=dz, mark=timer)
         if use_dist:
-            worker.reduce_update(dz_now[0])
+            worker.reduce_update(dz)
         eng.advance_epoch()
 
-    # K2 / K3 run one launch for the gate pairs and one for an odd last item
     n_items = eng.local * eng.S
+    # K2 / K3 run one launch for each chunk's gate pairs and one for an odd last item
     n_pairs = (n_items - (1 if eng.half is not None else 0)) // 2 * 2  # a half item is unpaired
-    per_kernel = int(n_pairs > 0) + int(n_items > n_pairs)
-    launches_per_step = 3 + 2 * per_kernel + ((2 if exchange == "p2p" else 1) if use_dist else 0)
+    tail = int(n_items > n_pairs)
+    n_chunks = len(chunks) if n_pairs > 0 else 0
+    launches_per_step = (max(n_chunks, 1) + 2 * (n_chunks + tail) + 2 +
+                         ((2 if exchange == "p2p" else 1) if use_dist else 0))
     for _ in range(args.warmup):
         step_fn()
     if use_dist and exchange == "p2p" and worker.p2p_failed_anywhere():
@@ -501,15 +487,14 @@ def run_ours(args, cfg):
         for _ in range(args.warmup):
             step_fn()
     hbm_peak, peak_src = peaks()
-    step_events = [[torch.cuda.Event(enable_timing=True) for _ in range(5)]
-                   for _ in range(args.steps)]
+    step_timers = [KernelTimer(torch, stream) for _ in range(args.steps)]
     barrier()
     with ClockSampler(local) as clocks:
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" selects it
         start.record(stream)
         for k in range(args.steps):
-            step_fn(step_events[k])
+            step_fn(step_timers[k])
         end.record(stream)
         torch.cuda.nvtx.range_pop()
         barrier()
@@ -522,8 +507,9 @@ def run_ours(args, cfg):
                           "primal": primal, "dual": dual}), file=sys.stderr)
     ms_step = ms_total / args.steps
     value = 1000.0 / ms_step
-    kern = {n: float(np.mean([ev[i].elapsed_time(ev[i + 1]) for ev in step_events]))
-            for i, n in enumerate(names)}
+    # per kernel, summed over the chunks of a step (engine.KernelTimer)
+    per_step = np.array([t.times_ms() for t in step_timers])
+    kern = {n: float(per_step[:, i].mean()) for i, n in enumerate(names)}
     items_per_launch = eng.local * eng.S
     ab = alg_bytes(cfg)
     iter_ms = sum(kern.values())
@@ -583,8 +569,6 @@ def run_ours(args, cfg):
             else:
                 runners.append(step_fn)
         eng.set_data_buffer(d_bufs[0])
-        if use_dist:
-            ip, sp = ctypes.byref(items), ctypes.byref(eng._st)  # re-bound state pointers
         eng.set_data_buffer(d_bufs[0])
         copy_s = torch.cuda.Stream()
         ev_done = [torch.cuda.Event(), torch.cuda.Event()]
@@ -684,7 +668,7 @@ def run_batch_ours(args, cfg):
     import paper_2410_10503_b200 as m
     from paper_2410_10503_b200 import _lib
     from paper_2410_10503_b200.distributed import slice_shard
-    from paper_2410_10503_b200.engine import Engine
+    from paper_2410_10503_b200.engine import Engine, KernelTimer
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -725,28 +709,15 @@ def run_batch_ours(args, cfg):
         return float(t.item())
 
     # per-kernel share: one eager epoch with events between the launches
-    L = _lib.load()
-    fam, ws, st = eng.family.handle, _lib.ptr(eng.ws), _lib.stream_handle(stream)
-    sp = ctypes.byref(eng._st)
     names = ["K1_prox_warp", "K2_forward_dual", "K3_adjoint", "K4_adjoint_update"]
-    kern = dict.fromkeys(names, 0.0)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(cfg.num_gates)]
+    timers = [KernelTimer(torch, stream) for _ in range(cfg.num_gates)]
     for k in range(cfg.num_gates):
-        items = eng.items_spdhg(k)
-        ip = ctypes.byref(items)
-        calls = [lambda: L.mct_iter_prox_warp(fam, ip, sp, eng.tau, cfg.alpha, ws, st),
-                 lambda: L.mct_iter_forward_dual(fam, ip, sp, ws, st),
-                 lambda: L.mct_iter_adjoint(fam, ip, ws, st),
-                 lambda: L.mct_iter_adjoint_update(fam, ip, sp, None, ws, st)]
-        for i, call in enumerate(calls):
-            evs[k][i].record(stream)
-            _lib.check(call())
-        evs[k][4].record(stream)
+        eng.iteration(eng.items_spdhg(k), cfg.alpha, mark=timers[k])
     eng.advance_epoch()
     torch.cuda.synchronize()
-    for k in range(cfg.num_gates):
-        for i, n_ in enumerate(names):
-            kern[n_] += evs[k][i].elapsed_time(evs[k][i + 1])
+    per_iter = np.array([t.times_ms() for t in timers])
+    kern = {n_: float(per_iter[:, i].sum()) for i, n_ in enumerate(names)}
+    chunks = eng.chunks(S, 0)
     eng.reset()
     g = eng.epoch_graph("spdhg", cfg.alpha)
     for _ in range(args.warmup):
@@ -846,7 +817,10 @@ def run_batch_ours(args, cfg):
             "e2e": e2e,
             "cpu_baseline": cpu,
             # per iteration: K1, K4 and K2 / K3 for the slice pairs (+ an odd last slice)
-            "gpu_launches": ((2 + 2 * (int(S >= 2) + S % 2)) * cfg.num_gates + 1) * args.steps,
+            # per iteration: K1 per chunk of the pair ring, K2 / K3 per chunk + an odd
+            # slice's single-item launch, K4; plus one counter bump per epoch
+            "gpu_launches": ((len(chunks) + 2 * ((len(chunks) if S >= 2 else 0) + S % 2) + 1)
+                             * cfg.num_gates + 1) * args.steps,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define MCT_ABI_VERSION 1
+#define MCT_ABI_VERSION 2
 
 #define MCT_OK 0
 #define MCT_ERR_ARG 1
@@ -58,10 +58,17 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
 int mct_ray_plan_destroy(mct_ray_plan* plan);
 
 /* Bytes of device workspace a standalone forward/adjoint call of up to `batch`
- * items needs (padded image copies + padded sinogram + image scratch per item,
- * plus one interleaved gate-pair region per item pair: launches of >= 2 items
- * process items 2p, 2p+1 together).  Not linear in `batch`; size with this.  */
+ * items needs: two single-item regions (padded image copies + padded sinogram +
+ * image scratch), a ring of interleaved gate-pair regions (launches of >= 2 items
+ * process items 2p, 2p+1 together; the ring holds at most about 256 MB, larger
+ * batches run through it chunk by chunk inside the call) and backprojection images
+ * per item.  A function of the plan and `batch` only; any call of <= `batch` items
+ * may use the workspace.  Not linear in `batch`; size with this.              */
 size_t mct_ray_workspace_bytes(const mct_ray_plan* plan, int batch);
+/* Most gate-pair regions a workspace of this plan holds (default: about 256 MB worth,
+ * at least 4).  Fewer regions = less memory, more (smaller) K1-K3 launches per
+ * iteration; results do not change.  Call before sizing any workspace.          */
+int mct_ray_plan_set_ring_pairs(mct_ray_plan* plan, int pairs);
 
 /* A: x_dev (batch, rows, cols) -> sino_dev (batch, A, B).  projector.py:201-207 */
 int mct_ray_forward(const mct_ray_plan* plan, const float* x_dev, float* sino_dev,
@@ -124,9 +131,14 @@ int mct_family_destroy(mct_family* fam);
 int mct_family_set_params(mct_family* fam, const double* sigmas, const double* probs,
                           double theta);
 
-/* Workspace bytes for launches of up to `items` (slice,gate) items (pair blocks,
- * see mct_ray_workspace_bytes).                                                */
+/* Workspace bytes for launches of up to `items` (slice,gate) items (see
+ * mct_ray_workspace_bytes).                                                    */
 size_t mct_family_workspace_bytes(const mct_family* fam, int items);
+/* Most items one K1-K3 chunk of a fused iteration of `items` items may hold (even;
+ * == items when every gate pair has its own region): launches with more items run
+ * K1 -> K2 -> K3 chunk after chunk (mct_items.first_item / item_count), then K4
+ * once.                                                                        */
+int mct_family_chunk_items(const mct_family* fam, int items);
 
 /* Standalone gated forward / adjoint of one (slice, gate): A(D x), D^*(A^* y). */
 int mct_gated_forward(const mct_family* fam, int slice, int gate, const float* x_dev,
@@ -175,6 +187,12 @@ typedef struct {
                                 covers only the first / second half of the angle pairs
                                 (half-gate units of gate-sharded PDHG, solvers.py has no
                                 counterpart: the partial images sum across ranks)   */
+    int32_t first_item;      /* K1-K3 only: this call covers items [first_item,
+                                first_item + item_count) of the launch (item_count 0:
+                                to the end); first_item a multiple of
+                                mct_family_chunk_items, item_count at most that.  K4
+                                takes 0 / 0 (it gathers every item).               */
+    int32_t item_count;
 } mct_items;
 
 /* Solver state buffers (device, fp32), slice-major.

@@ -37,6 +37,8 @@ class Items(ctypes.Structure):
         ("iteration", c_int32),
         ("iters_per_epoch", c_int32),
         ("last_part", c_int32),
+        ("first_item", c_int32),
+        ("item_count", c_int32),
     ]
 
 
@@ -63,6 +65,7 @@ SIGNATURES = {
                                     c_void_p]),
     "mct_ray_plan_destroy": (c_int, [c_void_p]),
     "mct_ray_workspace_bytes": (c_size_t, [c_void_p, c_int]),
+    "mct_ray_plan_set_ring_pairs": (c_int, [c_void_p, c_int]),
     "mct_ray_forward": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
     "mct_ray_adjoint": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
     "mct_warp_plan_create_rigid": (c_int, [PP, c_int, c_int, c_double, c_double, c_double,
@@ -79,6 +82,7 @@ SIGNATURES = {
     "mct_family_destroy": (c_int, [c_void_p]),
     "mct_family_set_params": (c_int, [c_void_p, c_void_p, c_void_p, c_double]),
     "mct_family_workspace_bytes": (c_size_t, [c_void_p, c_int]),
+    "mct_family_chunk_items": (c_int, [c_void_p, c_int]),
     "mct_gated_forward": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "mct_gated_adjoint": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "mct_iter_prox_warp": (c_int, [c_void_p, ctypes.POINTER(Items), ctypes.POINTER(State),
@@ -126,7 +130,7 @@ def load() -> ctypes.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.mct_abi_version() != 1:
+        if L.mct_abi_version() != 2:
             raise RuntimeError("unexpected mctomo_b200 ABI version")
         _LIB = L
     return _LIB

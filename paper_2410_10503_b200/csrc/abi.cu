@@ -52,6 +52,8 @@ ItemSel make_sel(const mct_items* it) {
     s.iteration = it->iteration;
     s.iters_per_epoch = it->iters_per_epoch;
     s.last_part = it->last_part;
+    s.first = it->first_item;
+    s.count = it->item_count;
     return s;
 }
 
@@ -72,6 +74,28 @@ int check_items(const mct_family* fam, const mct_items* it) {
     MCT_REQUIRE(it->last_part >= 0 && it->last_part <= 2, "items.last_part must be 0, 1 or 2");
     MCT_REQUIRE(it->last_part == 0 || it->num_slices == 1,
                 "a half last item needs a single-slice launch");
+    const int n = it->items_per_slice * it->num_slices;
+    MCT_REQUIRE(it->first_item >= 0 && it->first_item < n && (it->first_item & 1) == 0,
+                "items.first_item must be an even item index of the launch");
+    MCT_REQUIRE(it->item_count >= 0 && it->first_item + it->item_count <= n,
+                "items.item_count must be 0 (to the end) or end inside the launch");
+    return MCT_OK;
+}
+
+// K1-K3: the chunk's gate pairs must fit the workspace's ring of pair regions and
+// start on a ring boundary (mct_family_chunk_items)
+int check_chunk(const mct_family* fam, const mct_items* it) {
+    const int n = it->items_per_slice * it->num_slices;
+    const int np = mct_pair_items(n, it->last_part);
+    const int ring = fam->ray->wsg.ring;
+    const int end = it->item_count ? it->first_item + it->item_count : n;
+    const int p_lo = std::min(it->first_item, np), p_hi = std::min(end, np);
+    MCT_REQUIRE((p_hi - p_lo) / 2 <= ring,
+                "launch holds more gate pairs than the workspace's ring: run K1-K3 in chunks "
+                "of mct_family_chunk_items items (items.first_item / item_count)");
+    MCT_REQUIRE((p_lo / 2) % ring == 0, "items.first_item must be a multiple of the chunk size");
+    MCT_REQUIRE(it->item_count == 0 || end == n || (it->item_count & 1) == 0,
+                "a chunk that does not end the launch must hold whole gate pairs");
     return MCT_OK;
 }
 
@@ -122,6 +146,8 @@ AdjArgs adj_args(const mct_ray_plan* rp, const void* ws) {
     a.item0 = 0;
     a.n_items = 1;
     a.last_part = 0;
+    a.first = 0;
+    a.count = 0;
     a.asplit = 1;
     a.kfoot = rp->kfoot;
     a.segw = rp->adj_segw;
@@ -285,6 +311,8 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     poff += align256((size_t)num_angles * p->wy * sizeof(float4));
     p->wsg.pair_bytes = poff;
     p->wsg.pair_block = poff + 2 * p->wsg.pre_bytes;
+    p->wsg.ring = (int)std::max<long long>(MCT_RING_MIN_PAIRS,
+                                           (long long)((MCT_RING_BYTES + poff - 1) / poff));
 
     cudaError_t e = cudaMalloc(&p->d_fwd, sizeof(RayAngle) * num_angles);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_adj, sizeof(AdjAngle) * num_angles);
@@ -312,7 +340,14 @@ int mct_ray_plan_destroy(mct_ray_plan* plan) {
 
 size_t mct_ray_workspace_bytes(const mct_ray_plan* plan, int batch) {
     if (!plan || batch < 1) return 0;
-    return mct_ws_bytes(plan->wsg, batch);
+    return mct_ws_bytes(plan, batch);
+}
+
+int mct_ray_plan_set_ring_pairs(mct_ray_plan* plan, int pairs) {
+    MCT_REQUIRE(plan, "plan is null");
+    MCT_REQUIRE(pairs >= 1, "pairs must be >= 1");
+    plan->wsg.ring = pairs;
+    return MCT_OK;
 }
 
 int mct_ray_forward(const mct_ray_plan* rp, const float* x, float* sino, int batch, void* ws,
@@ -321,14 +356,18 @@ int mct_ray_forward(const mct_ray_plan* rp, const float* x, float* sino, int bat
     MCT_REQUIRE(batch >= 1, "batch must be >= 1");
     cudaStream_t st = (cudaStream_t)stream;
     PackArgs pa = pack_args(rp, ws);
-    pa.sel = single_sel(batch);
     pa.x = x;
-    MCT_CUDA(launch_pack(pa, batch, st), "pack");
     FwdArgs fa = fwd_args(rp, ws);
-    fa.sel = single_sel(batch);
     fa.out = sino;
     fa.out_item_stride = (long long)rp->A * rp->B;
-    MCT_CUDA(launch_fwd(fa, 0, batch, st), "ray forward");
+    const int chunk = mct_chunk_items(rp, batch);
+    for (int f = 0; f < batch; f += chunk) {  // chunks of the workspace's pair ring
+        pa.sel = fa.sel = single_sel(batch);
+        pa.sel.first = fa.sel.first = f;
+        pa.sel.count = fa.sel.count = f + chunk < batch ? chunk : 0;
+        MCT_CUDA(launch_pack(pa, batch, st), "pack");
+        MCT_CUDA(launch_fwd(fa, 0, batch, st), "ray forward");
+    }
     return MCT_OK;
 }
 
@@ -337,11 +376,17 @@ int mct_ray_adjoint(const mct_ray_plan* rp, const float* sino, float* img, int b
     MCT_REQUIRE(rp && sino && img && ws, "null argument");
     MCT_REQUIRE(batch >= 1, "batch must be >= 1");
     cudaStream_t st = (cudaStream_t)stream;
-    MCT_CUDA(launch_pad_sino(sino, rp, static_cast<char*>(ws), batch, st),
-             "pad sinogram");
     AdjArgs aa = adj_args(rp, ws);
     aa.asplit = choose_asplit(rp, batch);
-    MCT_CUDA(launch_adj(aa, rp->kfoot, batch, st), "ray adjoint");
+    const int chunk = mct_chunk_items(rp, batch);
+    for (int f = 0; f < batch; f += chunk) {  // chunks of the workspace's pair ring
+        aa.first = f;
+        aa.count = f + chunk < batch ? chunk : 0;
+        MCT_CUDA(launch_pad_sino(sino, rp, static_cast<char*>(ws), aa.wsg, batch, aa.first,
+                                 aa.count, st),
+                 "pad sinogram");
+        MCT_CUDA(launch_adj(aa, rp->kfoot, batch, st), "ray adjoint");
+    }
     UpdArgs ua = upd_args(rp, ws);
     ua.asplit = aa.asplit;
     ua.sel = single_sel(batch);
@@ -581,7 +626,12 @@ int mct_family_set_params(mct_family* fam, const double* sigmas, const double* p
 
 size_t mct_family_workspace_bytes(const mct_family* fam, int items) {
     if (!fam || items < 1) return 0;
-    return mct_ws_bytes(fam->ray->wsg, items);
+    return mct_ws_bytes(fam->ray, items);
+}
+
+int mct_family_chunk_items(const mct_family* fam, int items) {
+    if (!fam || items < 1) return 0;
+    return mct_chunk_items(fam->ray, items);
 }
 
 int mct_gated_forward(const mct_family* fam, int slice, int gate, const float* x, float* sino,
@@ -616,17 +666,21 @@ int mct_gated_forward_many(const mct_family* fam, int slice, const int32_t* gate
     sel.ips = count;
     sel.num_slices = 1;
     PackArgs pa = pack_args(rp, ws);
-    pa.sel = sel;
     pa.N = fam->N;
     pa.x = x;
     pa.warps = fam->d_warps + (size_t)slice * fam->N;
-    MCT_CUDA(launch_pack(pa, count, st), "gated pack (many)");
     FwdArgs fa = fwd_args(rp, ws);
-    fa.sel = sel;
     fa.ksplit = count > 1 ? 1 : rp->ksplit1;  // as the fused iteration (see MCT_KSPLIT_MIN)
     fa.out = sino;
     fa.out_item_stride = (long long)rp->A * rp->B;
-    MCT_CUDA(launch_fwd(fa, 0, count, st), "gated forward (many)");
+    const int chunk = mct_chunk_items(rp, count);
+    for (int f = 0; f < count; f += chunk) {
+        sel.first = f;
+        sel.count = f + chunk < count ? chunk : 0;
+        pa.sel = fa.sel = sel;
+        MCT_CUDA(launch_pack(pa, count, st), "gated pack (many)");
+        MCT_CUDA(launch_fwd(fa, 0, count, st), "gated forward (many)");
+    }
     return MCT_OK;
 }
 
@@ -636,9 +690,8 @@ int mct_gated_adjoint(const mct_family* fam, int slice, int gate, const float* y
     MCT_REQUIRE(slice >= 0 && slice < fam->S && gate >= 0 && gate < fam->N, "gate out of range");
     const mct_ray_plan* rp = fam->ray;
     cudaStream_t st = (cudaStream_t)stream;
-    MCT_CUDA(launch_pad_sino(y, rp, static_cast<char*>(ws), 1, st),
-             "pad sinogram");
     AdjArgs aa = adj_args(rp, ws);
+    MCT_CUDA(launch_pad_sino(y, rp, static_cast<char*>(ws), aa.wsg, 1, 0, 0, st), "pad sinogram");
     aa.asplit = choose_asplit(rp, 1);
     MCT_CUDA(launch_adj(aa, rp->kfoot, 1, st), "gated adjoint (A^*)");
     UpdArgs ua = upd_args(rp, ws);
@@ -657,6 +710,7 @@ int mct_iter_prox_warp(const mct_family* fam, const mct_items* it, mct_state* s,
     if (rc) return rc;
     MCT_REQUIRE(s && s->x && s->zbar && s->x_next && ws, "null state buffer");
     MCT_REQUIRE(tau >= 0 && alpha >= 0, "tau and alpha must be >= 0");
+    if ((rc = check_chunk(fam, it))) return rc;
     const mct_ray_plan* rp = fam->ray;
     PackArgs pa = pack_args(rp, ws);
     pa.sel = make_sel(it);
@@ -679,6 +733,7 @@ int mct_iter_forward_dual(const mct_family* fam, const mct_items* it, mct_state*
     if (rc) return rc;
     MCT_REQUIRE(fam->params_set, "mct_family_set_params has not been called");
     MCT_REQUIRE(s && s->y && s->d && ws, "null state buffer");
+    if ((rc = check_chunk(fam, it))) return rc;
     FwdArgs fa = fwd_args(fam->ray, ws);
     fa.ksplit = it->items_per_slice > 1 ? 1 : fam->ray->ksplit1;  // see MCT_KSPLIT_MIN
     fa.sel = make_sel(it);
@@ -697,9 +752,12 @@ int mct_iter_adjoint(const mct_family* fam, const mct_items* it, void* ws, void*
     int rc = check_items(fam, it);
     if (rc) return rc;
     MCT_REQUIRE(ws, "null workspace");
+    if ((rc = check_chunk(fam, it))) return rc;
     AdjArgs aa = adj_args(fam->ray, ws);
     const int items = it->items_per_slice * it->num_slices;
     aa.last_part = it->last_part;
+    aa.first = it->first_item;
+    aa.count = it->item_count;
     aa.asplit = choose_asplit(fam->ray, items, it->last_part);
     MCT_CUDA(launch_adj(aa, fam->ray->kfoot, items, (cudaStream_t)stream), "adjoint");
     return MCT_OK;
@@ -711,6 +769,8 @@ int mct_iter_adjoint_update(const mct_family* fam, const mct_items* it, mct_stat
     if (rc) return rc;
     MCT_REQUIRE(fam->params_set, "mct_family_set_params has not been called");
     MCT_REQUIRE(s && s->x && s->x_next && ws, "null state buffer");
+    MCT_REQUIRE(it->first_item == 0 && it->item_count == 0,
+                "K4 gathers every item of the launch: first_item / item_count must be 0");
     UpdArgs ua = upd_args(fam->ray, ws);
     ua.asplit = choose_asplit(fam->ray, it->items_per_slice * it->num_slices, it->last_part);
     ua.sel = make_sel(it);

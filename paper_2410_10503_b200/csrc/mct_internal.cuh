@@ -61,9 +61,10 @@ struct AdjAngle {
 
 struct WsGeom {
     size_t item_bytes;  // a single region
-    size_t pre_bytes;   // A^* IMG slots (prefix of an item region)
+    size_t pre_bytes;   // A^* IMG slots (prefix of a single region / of a pair block's item)
     size_t pair_bytes;  // interleaved X / XT / DY of a gate pair
     size_t pair_block;  // pair_bytes + 2 * pre_bytes
+    int ring;           // pair blocks a workspace holds at most (see mct_pair_off)
 };
 struct mct_ray_plan {
     int rows, cols, A, B;
@@ -132,31 +133,54 @@ __host__ __device__ __forceinline__ int mct_pair_items(int items, int last_part)
 // [1, 1 + P/2), part 2 = pairs q in [1 + P/2, P + 1), P = (A-1)/2.
 __host__ __device__ __forceinline__ int mct_half_q(int A) { return 1 + ((A - 1) / 2) / 2; }
 
-// Workspace layout (one per launch family; every region keeps one role for every
-// launch size, so pads zeroed once stay zero):
-//   [single region 0 | single region 1 | pair block 0 | pair block 1 | ...]
+// Workspace layout (one per launch family; a function of the plan alone, so every
+// region keeps one role for every launch size and pads zeroed once stay zero):
+//   [single region 0 | single region 1 | pair block 0 .. ring-1 | overflow IMG area]
 // A single region (item_bytes) is the full item layout (A^* IMG slots, then the K2
 // ray-split partials and arrival counters and the X / XT / DY of the mirror
 // kernels) of an unpaired item: unpaired item k of a launch (k = item - pair_items,
 // at most two: an odd last item and / or a half item) uses single region k.  Pair
 // block p is the interleaved pair region (X / XT / DY of items 2p, 2p+1,
-// pair_bytes) followed by the two items' *prefixes* (pre_bytes: the IMG slots) --
+// pair_bytes) followed by the two items' prefixes (pre_bytes: the IMG slots) --
 // gate-pair K2 launches never split rays and paired items never touch the
 // single-item X / XT / DY, so a pair block holds no copy of them.
+// A workspace holds at most `ring` pair blocks (about MCT_RING_BYTES of pair regions,
+// >= MCT_RING_MIN_PAIRS).  Launches with more pairs run K1 -> K2 -> K3 chunk by chunk
+// of `ring` pairs (mct_items.first_item / item_count): pair p uses the pair region of
+// block p % ring, so the X / XT / DY of a chunk are dead before the next chunk
+// overwrites them (same elements, pads untouched).  The A^* partial images outlive
+// the chunks (K4 gathers all of them): items of pairs >= ring keep theirs in the
+// overflow area behind the blocks, item i, split k of a call with angle split s at
+// slot (i - 2 ring) * s + k (no pads, rewritten by every call).
+#ifndef MCT_RING_BYTES
+#define MCT_RING_BYTES (256ull << 20)
+#endif
+#ifndef MCT_RING_MIN_PAIRS
+#define MCT_RING_MIN_PAIRS 4
+#endif
 __host__ __device__ __forceinline__ size_t mct_pair_off(int pair, const WsGeom& g) {
-    return 2 * g.item_bytes + (size_t)pair * g.pair_block;
+    return 2 * g.item_bytes + (size_t)(pair % g.ring) * g.pair_block;
 }
-// Byte offset of item `item`'s region (paired: its prefix) in a launch whose
-// items [0, pair_items) run the gate-pair kernels.
+// Byte offset of item `item`'s region in a launch whose items [0, pair_items) run
+// the gate-pair kernels (paired: the pair region).
 __host__ __device__ __forceinline__ size_t mct_item_off(int item, int pair_items,
                                                         const WsGeom& g) {
-    return item < pair_items ? mct_pair_off(item >> 1, g) + g.pair_bytes + (item & 1) * g.pre_bytes
+    return item < pair_items ? mct_pair_off(item >> 1, g)
                              : (size_t)(item - pair_items) * g.item_bytes;
 }
-// Workspace bytes for launches of up to `items` items.
-inline size_t mct_ws_bytes(const WsGeom& g, int items) {
-    return items <= 1 ? g.item_bytes : 2 * g.item_bytes + (size_t)(items / 2) * g.pair_block;
+// Byte offset of item `item`'s first A^* partial-image slot (the call's asplit slots
+// follow one another, slot_bytes apart).
+__host__ __device__ __forceinline__ size_t mct_img_off(int item, int pair_items, int asplit,
+                                                       size_t slot_bytes, const WsGeom& g) {
+    if (item >= pair_items) return (size_t)(item - pair_items) * g.item_bytes;
+    if (item < 2 * g.ring) return mct_pair_off(item >> 1, g) + g.pair_bytes + (item & 1) * g.pre_bytes;
+    return 2 * g.item_bytes + (size_t)g.ring * g.pair_block +
+           (size_t)(item - 2 * g.ring) * asplit * slot_bytes;
 }
+// Workspace bytes for launches of up to `items` items, and the most items one K1-K3
+// chunk may hold (ray_kernels.cu).
+size_t mct_ws_bytes(const struct mct_ray_plan* rp, int items);
+int mct_chunk_items(const struct mct_ray_plan* rp, int items);
 
 // --------------------------------------------------------------- warp plan --
 struct WarpDesc {
@@ -201,6 +225,7 @@ struct ItemSel {
     const int* epoch_ctr;
     int slice_stride, epoch_stride, base, ips, num_slices, iteration, iters_per_epoch;
     int last_part;  // 0, or 1 / 2: the launch's last item covers the first / second half
+    int first, count;  // K1-K3 chunk: items [first, first + count) (count 0: to the end)
 };
 
 __device__ __forceinline__ void resolve_item(const ItemSel& s, int item, int& slice, int& gate,
@@ -268,6 +293,7 @@ struct AdjArgs {
     size_t off_pdy;
     int item0;               // first item of the launch
     int n_items, last_part;  // items of the whole call; see ItemSel::last_part
+    int first, count;        // K1-K3 chunk, see ItemSel
     int asplit;
     int kfoot;               // adjoint footprint (bins thi-kfoot .. thi+kfoot+1)
     int segw;                // staged sinogram segment length (K = 0, ADJ_TMA)
@@ -294,8 +320,8 @@ struct UpdArgs {
 
 // ------------------------------------------------------------- launchers --
 cudaError_t launch_pack(const PackArgs& a, int items, cudaStream_t st);
-cudaError_t launch_pad_sino(const float* sino, const mct_ray_plan* rp, char* ws, int items,
-                            cudaStream_t st);
+cudaError_t launch_pad_sino(const float* sino, const mct_ray_plan* rp, char* ws,
+                            const WsGeom& wsg, int items, int first, int count, cudaStream_t st);
 cudaError_t launch_fwd(const FwdArgs& a, int mode, int items, cudaStream_t st);
 cudaError_t launch_adj(const AdjArgs& a, int kfoot, int items, cudaStream_t st);  // a.last_part
 int choose_asplit(const mct_ray_plan* rp, int items, int last_part = 0);

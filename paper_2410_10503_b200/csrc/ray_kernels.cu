@@ -44,7 +44,7 @@ template <int T, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) pack_kernel(PackArgs p) {
     constexpr int HR = T + 1, HC = T + 2;  // rows r0 .. r0+T, cols c0-1 .. c0+T
     __shared__ float tile[HR][HC + 1];
-    const int item = blockIdx.z;
+    const int item = p.sel.first + blockIdx.z;
     int slice, gate, iter;
     resolve_item(p.sel, item, slice, gate, iter);
     const int k_in_slice = item - slice * p.sel.ips;
@@ -137,8 +137,9 @@ __global__ void __launch_bounds__(THREADS, MINB) pack_kernel(PackArgs p) {
 // the mirror layout of their own region (row / slot of mir_row_slot).
 __global__ void pad_sino_kernel(const float* __restrict__ sino, const AdjAngle* __restrict__ ang,
                                 char* ws, WsGeom wsg, size_t off_dy1,
-                                size_t off_dy2, int A, int B, int wy, int pb, int pair_items) {
-    const int item = blockIdx.z;
+                                size_t off_dy2, int A, int B, int wy, int pb, int pair_items,
+                                int first) {
+    const int item = first + blockIdx.z;
     const bool paired = item < pair_items;
     const int a = blockIdx.y;
     const float step = ang[a].step;
@@ -259,10 +260,10 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
     const bool active = warp_on && j < p.B;
     const int jj = active ? j : p.B - 1;  // idle lanes shadow the last bin (no store)
     const RayAngle ra = p.ang[a];
-    const int item0 = MIR ? p.item0 + group : G * group;  // pair launches start at item 0
+    const int item0 = p.item0 + (MIR ? group : G * group);  // pairs: item0 is even
     const int np = mct_pair_items(p.n_items, p.sel.last_part);  // paired items of the call
     const char* base0 = p.ws + mct_item_off(item0, np, p.wsg);  // counters
-    const char* tb = MIR ? base0 : p.ws + mct_pair_off(group, p.wsg);
+    const char* tb = MIR ? base0 : p.ws + mct_pair_off(item0 >> 1, p.wsg);
     const int cd = ra.cols_dom;
     // tap index = hi(fx) >= 0: the row pad is folded into fx so the address is one
     // unsigned 32x64 multiply-add
@@ -977,8 +978,9 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
 #pragma unroll
     for (int h = 0; h < G; ++h) {
         float* IMG = reinterpret_cast<float*>(
-            const_cast<char*>(p.ws) + mct_item_off(item0 + h, np, p.wsg) +
-            p.off_img + (size_t)split * p.img_slot_bytes);
+            const_cast<char*>(p.ws) +
+            mct_img_off(item0 + h, np, p.asplit, p.img_slot_bytes, p.wsg) + p.off_img +
+            (size_t)split * p.img_slot_bytes);
         for (int m = 0; m < nrows; ++m) {
             const long long row = (long long)(rt + RSTEP * m) * p.cols;
             if (cm == c) {  // centre column of an odd width: the primary role already
@@ -1008,22 +1010,23 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
 cudaError_t launch_pack(const PackArgs& a_in, int items, cudaStream_t st) {
     PackArgs a = a_in;
     a.pair_items = mct_pair_items(items, a.sel.last_part);
+    const int n = a.sel.count ? a.sel.count : items - a.sel.first;  // this chunk
     if (items <= PACK_SMALL_ITEMS) {  // few gates: small tiles, one halo element per thread
-        dim3 grid((a.cols + 15) / 16, (a.rows + 15) / 16, items);
+        dim3 grid((a.cols + 15) / 16, (a.rows + 15) / 16, n);
         pack_kernel<16, 320, PACK16_MINB><<<grid, 320, 0, st>>>(a);
     } else {
-        dim3 grid((a.cols + 31) / 32, (a.rows + 31) / 32, items);
+        dim3 grid((a.cols + 31) / 32, (a.rows + 31) / 32, n);
         pack_kernel<32, PACK32_THREADS, PACK32_MINB><<<grid, PACK32_THREADS, 0, st>>>(a);
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_pad_sino(const float* sino, const mct_ray_plan* rp, char* ws, int items,
-                            cudaStream_t st) {
-    dim3 block(256), grid((rp->B + 255) / 256, rp->A, items);
-    pad_sino_kernel<<<grid, block, 0, st>>>(sino, rp->d_adj, ws, rp->wsg,
+cudaError_t launch_pad_sino(const float* sino, const mct_ray_plan* rp, char* ws,
+                            const WsGeom& wsg, int items, int first, int count, cudaStream_t st) {
+    dim3 block(256), grid((rp->B + 255) / 256, rp->A, count ? count : items - first);
+    pad_sino_kernel<<<grid, block, 0, st>>>(sino, rp->d_adj, ws, wsg,
                                             rp->off_dy, rp->off_pdy, rp->A, rp->B, rp->wy, rp->pb,
-                                            mct_pair_items(items));
+                                            mct_pair_items(items), first);
     return cudaGetLastError();
 }
 
@@ -1129,13 +1132,17 @@ cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st
     const dim3 block(32, FWD_ANGLES);
     const unsigned ntile = mct_fwd_btiles(a_in.B);
     const int np = mct_pair_items(items, a_in.sel.last_part);
+    // this chunk's paired items [p_lo, p_hi); the unpaired tail runs with the last chunk
+    const int first = a_in.sel.first, end = a_in.sel.count ? first + a_in.sel.count : items;
+    const int p_lo = first < np ? first : np, p_hi = end < np ? end : np;
+    const bool tail = end == items && items > np;
     // gate pairs (bins fastest: L2 locality across pairs)
     auto pairs = [&](cudaStream_t s) {
         FwdArgs a = a_in;
-        a.item0 = 0;
+        a.item0 = p_lo;
         a.n_items = items;
         a.ksplit = 1;  // >= 2 items fill the GPU without splitting rays (no partials)
-        dim3 grid(ntile, mct_fwd_groups(a.A), (np / 2) * a.ksplit);
+        dim3 grid(ntile, mct_fwd_groups(a.A), ((p_hi - p_lo) / 2) * a.ksplit);
         if (mode == 0)
             fwd_kernel<0, 0, 0><<<grid, block, 0, s>>>(a);
         else
@@ -1164,11 +1171,9 @@ cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st
             fwd_kernel<1, 0, 1><<<grid, block, 0, s>>>(a);
         }
     };
-    if (np > 0 && items > np) return fork_join(st, pairs, singles);
-    if (np > 0)
-        pairs(st);
-    else
-        singles(st);
+    if (p_hi > p_lo && tail) return fork_join(st, pairs, singles);
+    if (p_hi > p_lo) pairs(st);
+    if (tail) singles(st);
     return cudaGetLastError();
 }
 
@@ -1336,11 +1341,14 @@ static void launch_adj_g(const AdjArgs& a, int kfoot, int groups, cudaStream_t s
 cudaError_t launch_adj(const AdjArgs& a_in, int kfoot, int items, cudaStream_t st) {
     if (kfoot < 0) return cudaErrorInvalidValue;
     const int np = mct_pair_items(items, a_in.last_part);
+    const int first = a_in.first, end = a_in.count ? first + a_in.count : items;
+    const int p_lo = first < np ? first : np, p_hi = end < np ? end : np;
+    const bool tail = end == items && items > np;
     auto pairs = [&](cudaStream_t s) {
         AdjArgs a = a_in;
-        a.item0 = 0;
+        a.item0 = p_lo;
         a.n_items = items;
-        launch_adj_g<2>(a, kfoot, np / 2, s);
+        launch_adj_g<2>(a, kfoot, (p_hi - p_lo) / 2, s);
     };
     auto singles = [&](cudaStream_t s) {
         AdjArgs a = a_in;
@@ -1348,10 +1356,35 @@ cudaError_t launch_adj(const AdjArgs& a_in, int kfoot, int items, cudaStream_t s
         a.n_items = items;
         launch_adj_g<1>(a, kfoot, items - np, s);
     };
-    if (np > 0 && items > np) return fork_join(st, pairs, singles);  // concurrent
-    if (np > 0)
-        pairs(st);
-    else
-        singles(st);
+    if (p_hi > p_lo && tail) return fork_join(st, pairs, singles);  // concurrent
+    if (p_hi > p_lo) pairs(st);
+    if (tail) singles(st);
     return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- workspace
+// (layout: mct_internal.cuh)
+int mct_chunk_items(const mct_ray_plan* rp, int items) {
+    return items / 2 > rp->wsg.ring ? 2 * rp->wsg.ring : items;
+}
+
+size_t mct_ws_bytes(const mct_ray_plan* rp, int items) {
+    const WsGeom& g = rp->wsg;
+    if (items <= 1) return g.item_bytes;
+    const int pairs = items / 2;
+    size_t bytes = 2 * g.item_bytes + (size_t)(pairs < g.ring ? pairs : g.ring) * g.pair_block;
+    if (pairs > g.ring) {
+        // overflow IMG area: the most slots any launch of <= items items needs beyond
+        // the blocks' own (its paired items past the ring x its angle split; a half
+        // last item changes both)
+        long long slots = 0;
+        for (int n = 2 * g.ring + 2; n <= items; ++n)
+            for (int part = 0; part <= 1; ++part) {
+                const long long over = mct_pair_items(n, part) - 2 * g.ring;
+                const long long s = over * choose_asplit(rp, n, part);
+                slots = s > slots ? s : slots;
+            }
+        bytes += (size_t)slots * rp->img_slot_bytes;
+    }
+    return bytes;
 }

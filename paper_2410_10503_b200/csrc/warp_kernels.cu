@@ -59,7 +59,8 @@ update_kernel(UpdArgs p) {
         resolve_item(p.sel, item, s_, gate, iter);
         const char* img = p.img_override
                               ? reinterpret_cast<const char*>(p.img_override)
-                              : p.ws + mct_item_off(item, np, p.wsg) + p.off_img;
+                              : p.ws + mct_img_off(item, np, p.asplit, p.img_slot_bytes, p.wsg) +
+                                    p.off_img;
         const int asplit = p.asplit;
         const size_t slot = p.img_slot_bytes;
         // sum of the adjoint's partial-image slots, fixed order (loads four at a time)

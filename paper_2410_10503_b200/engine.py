@@ -86,6 +86,33 @@ class Family:
             pass
 
 
+class KernelTimer:
+    """CUDA-event marks between the kernels of ``Engine.iteration`` (measurement only):
+    ``times_ms()`` sums, per kernel K1..K4, the event time from each of its marks to the
+    next mark (a chunked launch marks K1-K3 once per chunk)."""
+
+    def __init__(self, torch, stream=None):
+        self.torch = torch
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        self.marks = []
+
+    def __call__(self, index: int):
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record(self.stream)
+        self.marks.append((index, ev))
+
+    def times_ms(self):
+        out = [0.0, 0.0, 0.0, 0.0]
+        for (i, a), (_, b) in zip(self.marks, self.marks[1:]):
+            if i < 4:
+                out[i] += a.elapsed_time(b)
+        return out
+
+    def launches(self):
+        """Marks per kernel (the K1-K3 chunk count shows up here)."""
+        return [sum(1 for i, _ in self.marks if i == k) for k in range(4)]
+
+
 class Engine:
     """Fused-iteration executor for S slices sharing one geometry and gate count."""
 
@@ -148,6 +175,9 @@ class Engine:
         self.max_items = items
         self.ws = torch.zeros(int(_lib.load().mct_family_workspace_bytes(self.family.handle, items)),
                               dtype=torch.uint8, device=dev)
+        # launches with more gate pairs than the workspace's ring of pair regions run
+        # K1 -> K2 -> K3 in chunks of this many items (mct_family_chunk_items)
+        self.chunk_items = int(_lib.load().mct_family_chunk_items(self.family.handle, items))
         self.all_gates = torch.arange(self.N, dtype=torch.int32, device=dev)
         self.local_gates = (None if self.half is None else torch.tensor(
             list(range(self.gate_lo, self.gate_hi)) + [self.half[0]], dtype=torch.int32,
@@ -238,18 +268,43 @@ class Engine:
         return it
 
     # ------------------------------------------------------------ iteration
-    def iteration(self, items: _lib.Items, alpha: float, dz=None):
-        """K1..K4 of one iteration on the current stream."""
+    def iteration(self, items: _lib.Items, alpha: float, dz=None, mark=None):
+        """K1..K4 of one iteration on the current stream.  ``mark(i)`` (a
+        ``KernelTimer``) is called before kernel i = 0..3 and ``mark(4)`` at the end."""
         L = _lib.load()
         fam = self.family.handle
         ws = _lib.ptr(self.ws)
         st = _lib.stream_handle()
         ip, sp = ctypes.byref(items), ctypes.byref(self._st)
-        _lib.check(L.mct_iter_prox_warp(fam, ip, sp, self.tau, float(alpha), ws, st))
-        _lib.check(L.mct_iter_forward_dual(fam, ip, sp, ws, st))
-        _lib.check(L.mct_iter_adjoint(fam, ip, ws, st))
+        n = items.items_per_slice * items.num_slices
+        for first, count in self.chunks(n, items.last_part):
+            items.first_item, items.item_count = first, count
+            if mark is not None:
+                mark(0)
+            _lib.check(L.mct_iter_prox_warp(fam, ip, sp, self.tau, float(alpha), ws, st))
+            if mark is not None:
+                mark(1)
+            _lib.check(L.mct_iter_forward_dual(fam, ip, sp, ws, st))
+            if mark is not None:
+                mark(2)
+            _lib.check(L.mct_iter_adjoint(fam, ip, ws, st))
+        items.first_item = items.item_count = 0
+        if mark is not None:
+            mark(3)
         _lib.check(L.mct_iter_adjoint_update(fam, ip, sp, _lib.ptr(dz) if dz is not None else None,
                                              ws, st))
+        if mark is not None:
+            mark(4)
+
+    def chunks(self, n: int, last_part: int = 0):
+        """(first_item, item_count) of the K1-K3 chunks of an n-item launch: whole gate
+        pairs, at most ``chunk_items`` per chunk; the unpaired tail (an odd or half last
+        item) rides with the last chunk (item_count 0 = to the end)."""
+        paired = (n - 1 if last_part else n) & ~1
+        c = self.chunk_items
+        if paired <= c:
+            return [(0, 0)]
+        return [(f, c if f + c < paired else 0) for f in range(0, paired, c)]
 
     def z_update(self, dz, theta: float):
         _lib.check(_lib.load().mct_iter_z_update(self.family.handle, ctypes.byref(self._st),

@@ -105,6 +105,12 @@ class _RayPlan:
         """Workspace bytes for launches of up to `items` items (gate-pair blocks)."""
         return int(_lib.load().mct_ray_workspace_bytes(self.handle, int(items)))
 
+    def set_ring_pairs(self, pairs: int) -> None:
+        """Cap the gate-pair regions a workspace of this plan holds (less memory, more
+        K1-K3 chunks per iteration, same results).  Call before any workspace or engine
+        of this plan exists: the workspace layout follows it."""
+        _lib.check(_lib.load().mct_ray_plan_set_ring_pairs(self.handle, int(pairs)))
+
     def __del__(self):
         try:
             if self.handle:

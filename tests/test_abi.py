@@ -24,7 +24,7 @@ def test_library_builds_and_loads():
     build_native()
     assert LIB_PATH.exists()
     L = _lib.load()
-    assert L.mct_abi_version() == 1
+    assert L.mct_abi_version() == 2
 
 
 def test_every_declared_symbol_is_exported_and_bound():

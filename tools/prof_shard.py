@@ -15,7 +15,7 @@ import torch  # noqa: E402
 
 import paper_2410_10503_b200 as m  # noqa: E402
 from paper_2410_10503_b200 import _lib, workloads  # noqa: E402
-from paper_2410_10503_b200.engine import Engine  # noqa: E402
+from paper_2410_10503_b200.engine import Engine, KernelTimer  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
@@ -43,25 +43,16 @@ for kk in args.locals.split(","):
     eng.reset()
     dz = torch.zeros_like(eng.x)
     items = eng.items_pdhg(epoch_ctr=True)
-    ip, sp = ctypes.byref(items), ctypes.byref(eng._st)
-    fam, ws, st = eng.family.handle, _lib.ptr(eng.ws), _lib.stream_handle()
-    calls = [lambda: L.mct_iter_prox_warp(fam, ip, sp, eng.tau, cfg.alpha, ws, st),
-             lambda: L.mct_iter_forward_dual(fam, ip, sp, ws, st),
-             lambda: L.mct_iter_adjoint(fam, ip, ws, st),
-             lambda: L.mct_iter_adjoint_update(fam, ip, sp, _lib.ptr(dz), ws, st)]
     per = []
     for it in range(args.iters + 3):
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-        for i, call in enumerate(calls):
-            evs[i].record(stream)
-            _lib.check(call())
-        evs[4].record(stream)
+        timer = KernelTimer(torch, stream)
+        eng.iteration(items, cfg.alpha, dz=dz, mark=timer)
         eng.z_update(dz, c.theta)
         eng.advance_epoch()
         if it >= 3:
-            per.append(evs)
+            per.append(timer)
     torch.cuda.synchronize()
-    t = np.array([[e[i].elapsed_time(e[i + 1]) for i in range(4)] for e in per])
+    t = np.array([tm.times_ms() for tm in per])
     med = np.median(t, 0)
     out[kk] = {"K1": round(float(med[0]) * 1e3, 1), "K2": round(float(med[1]) * 1e3, 1),
               "K3": round(float(med[2]) * 1e3, 1), "K4": round(float(med[3]) * 1e3, 1),

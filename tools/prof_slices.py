@@ -16,7 +16,7 @@ import torch  # noqa: E402
 
 import paper_2410_10503_b200 as m  # noqa: E402
 from paper_2410_10503_b200 import _lib, workloads  # noqa: E402
-from paper_2410_10503_b200.engine import Engine  # noqa: E402
+from paper_2410_10503_b200.engine import Engine, KernelTimer  # noqa: E402
 
 cfg = workloads.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c3"]
 SLICES = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1, 2, 4, 8]
@@ -36,33 +36,19 @@ for S in SLICES:
     eng.reset()
     eng.set_sequences(np.stack([m.draw_sequence(c, 60 * cfg.num_gates)] * S))
     stream = torch.cuda.current_stream()
-    fam, ws, st = eng.family.handle, _lib.ptr(eng.ws), _lib.stream_handle()
-    sp = ctypes.byref(eng._st)
 
-    def iteration(k, evs=None):
-        items = eng.items_spdhg(k)
-        ip = ctypes.byref(items)
-        calls = [lambda: L.mct_iter_prox_warp(fam, ip, sp, eng.tau, cfg.alpha, ws, st),
-                 lambda: L.mct_iter_forward_dual(fam, ip, sp, ws, st),
-                 lambda: L.mct_iter_adjoint(fam, ip, ws, st),
-                 lambda: L.mct_iter_adjoint_update(fam, ip, sp, None, ws, st)]
-        for i, call in enumerate(calls):
-            if evs is not None:
-                evs[i].record(stream)
-            _lib.check(call())
-        if evs is not None:
-            evs[4].record(stream)
+    def iteration(k, timer=None):
+        eng.iteration(eng.items_spdhg(k), cfg.alpha, mark=timer)
 
     for k in range(2 * cfg.num_gates):
         iteration(k % cfg.num_gates)
     torch.cuda.synchronize()
     K = 2 * cfg.num_gates
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
+    timers = [KernelTimer(torch, stream) for _ in range(K)]
     for k in range(K):
-        iteration(k % cfg.num_gates, evs[k])
+        iteration(k % cfg.num_gates, timers[k])
     torch.cuda.synchronize()
-    per = np.median([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(4)]
-                     for k in range(K)], axis=0)
+    per = np.median([t.times_ms() for t in timers], axis=0)
     out[S] = {n: round(1000 * float(v) / S, 1) for n, v in zip(("K1", "K2", "K3", "K4"), per)}
     out[S]["sum"] = round(sum(out[S][n] for n in ("K1", "K2", "K3", "K4")), 1)
     del eng

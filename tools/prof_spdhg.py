@@ -25,7 +25,7 @@ import torch  # noqa: E402
 
 import paper_2410_10503_b200 as m  # noqa: E402
 from paper_2410_10503_b200 import _lib, workloads  # noqa: E402
-from paper_2410_10503_b200.engine import Engine  # noqa: E402
+from paper_2410_10503_b200.engine import Engine, KernelTimer  # noqa: E402
 
 cfg = workloads.CONFIGS[args.config]
 inp = workloads.slice_inputs(cfg, 0)
@@ -43,36 +43,21 @@ eng.set_sequences(m.draw_sequence(c)[None])
 L = _lib.load()
 N = cfg.num_gates
 stream = torch.cuda.current_stream()
-fam, ws, st = eng.family.handle, _lib.ptr(eng.ws), _lib.stream_handle()
-sp = ctypes.byref(eng._st)
 
 
-def iteration(k, evs=None):
-    items = eng.items_spdhg(k)
-    ip = ctypes.byref(items)
-    calls = [
-        lambda: L.mct_iter_prox_warp(fam, ip, sp, eng.tau, cfg.alpha, ws, st),
-        lambda: L.mct_iter_forward_dual(fam, ip, sp, ws, st),
-        lambda: L.mct_iter_adjoint(fam, ip, ws, st),
-        lambda: L.mct_iter_adjoint_update(fam, ip, sp, None, ws, st),
-    ]
-    for i, call in enumerate(calls):
-        if evs is not None:
-            evs[i].record(stream)
-        _lib.check(call())
-    if evs is not None:
-        evs[4].record(stream)
+def iteration(k, timer=None):
+    eng.iteration(eng.items_spdhg(k), cfg.alpha, mark=timer)
 
 
 for k in range(2 * N):
     iteration(k % N)
 torch.cuda.synchronize()
 K = args.epochs * N
-evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
+timers = [KernelTimer(torch, stream) for _ in range(K)]
 for k in range(K):
-    iteration(k % N, evs[k])
+    iteration(k % N, timers[k])
 torch.cuda.synchronize()
-per = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(4)] for k in range(K)])
+per = np.array([t.times_ms() for t in timers])
 eng.reset()
 g = eng.epoch_graph("spdhg", cfg.alpha)
 for _ in range(3):
