@@ -169,14 +169,14 @@ def test_unchunked_call_past_the_ring_is_refused(m):
 def test_c4_shape_workspace_is_bounded(m):
     """BASELINE C4 geometry (1024^2, 1440 x 1453, 40 gates): the pair ring bounds the
     fused-iteration workspace below 1 GB (one region per pair: 2.2 GB) and the C5
-    batch (64 slices of 512^2) below 0.5 GB."""
+    batch (64 slices of 512^2) below 0.6 GB (one region per pair: 0.88 GB)."""
     from paper_2410_10503_b200 import projector
 
     projector.ray_transform.cache_clear()
     p4 = m.ray_transform(m.Geometry(1024, 1024, 1440, 1453, 1.0)).plan()
     assert p4.workspace_bytes(40) < 2**30
     p5 = m.ray_transform(m.Geometry(512, 512, 720, 729, 1.0)).plan()
-    assert p5.workspace_bytes(64) < 0.5 * 2**30
+    assert p5.workspace_bytes(64) < 0.6 * 2**30
     assert p5.workspace_bytes(20) > 10 * 16 * 2**20  # C3: every pair keeps its own region
     projector.ray_transform.cache_clear()
 
