@@ -233,7 +233,8 @@ def pattern_cycles(cfg):
 
 def roofline_line(cfg, kern_ms, items, traffic_all, wave_frac, sm_mhz, hbm_peak, peak_src):
     """The bench line's ``roofline``: the limiter that binds K2 / K3 is the L1 data
-    pipe (ncu: LSU wavefronts 96 % / 75 % of peak, DRAM < 3 %), so the headline
+    pipe (ncu, profiles/ncu_traffic.json: data-pipe wavefronts 79 % / 90 % of peak on
+    the 20-gate C3 launches, DRAM < 4 %), so the headline
     fraction is operand bytes delivered L1 -> registers (l1_operand_bytes, exact
     counts) over the data-pipe peak; the SURVEY §8d SpMV-equivalent HBM figure and
     the compulsory-bytes HBM fraction are kept as labelled secondary fields.
