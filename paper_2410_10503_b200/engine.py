@@ -86,6 +86,20 @@ class Family:
             pass
 
 
+def chunk_plan(n: int, last_part: int, chunk_items: int):
+    """(first_item, item_count) of the K1-K3 chunks of an n-item launch through a
+    workspace whose pair ring holds ``chunk_items`` items (mct_family_chunk_items):
+    whole gate pairs, at most ``chunk_items`` per chunk; the unpaired tail (an odd or
+    half last item) rides with the last chunk (item_count 0 = to the end)."""
+    paired = (n - 1 if last_part else n) & ~1
+    c = int(chunk_items)
+    if paired <= c:
+        return [(0, 0)]
+    if c < 2 or c % 2:
+        raise ValueError("a chunk holds whole gate pairs: chunk_items must be even and >= 2")
+    return [(f, c if f + c < paired else 0) for f in range(0, paired, c)]
+
+
 class KernelTimer:
     """CUDA-event marks between the kernels of ``Engine.iteration`` (measurement only):
     ``times_ms()`` sums, per kernel K1..K4, the event time from each of its marks to the
@@ -297,14 +311,8 @@ class Engine:
             mark(4)
 
     def chunks(self, n: int, last_part: int = 0):
-        """(first_item, item_count) of the K1-K3 chunks of an n-item launch: whole gate
-        pairs, at most ``chunk_items`` per chunk; the unpaired tail (an odd or half last
-        item) rides with the last chunk (item_count 0 = to the end)."""
-        paired = (n - 1 if last_part else n) & ~1
-        c = self.chunk_items
-        if paired <= c:
-            return [(0, 0)]
-        return [(f, c if f + c < paired else 0) for f in range(0, paired, c)]
+        """(first_item, item_count) of the K1-K3 chunks of an n-item launch."""
+        return chunk_plan(n, last_part, self.chunk_items)
 
     def z_update(self, dz, theta: float):
         _lib.check(_lib.load().mct_iter_z_update(self.family.handle, ctypes.byref(self._st),

@@ -195,3 +195,32 @@ def test_helper_maps_validation_and_no_fallback():
     if not torch.cuda.is_available():
         with pytest.raises(RuntimeError, match="CUDA"):
             s.apply(np.zeros((3, 4)))
+
+
+def test_chunk_plan_of_the_pair_ring():
+    """K1-K3 chunks of a launch through a workspace whose pair ring holds `chunk_items`
+    items (engine.chunk_plan): whole gate pairs, the unpaired tail (an odd
+    or a half last item) with the last chunk, (0, 0) when everything fits."""
+    from paper_2410_10503_b200.engine import chunk_plan
+
+    assert chunk_plan(1, 0, 1) == [(0, 0)]
+    assert chunk_plan(20, 0, 20) == [(0, 0)]          # C3: every pair has its region
+    assert chunk_plan(7, 0, 7) == [(0, 0)]
+    assert chunk_plan(40, 0, 8) == [(0, 8), (8, 8), (16, 8), (24, 8), (32, 0)]  # C4
+    assert chunk_plan(64, 0, 32) == [(0, 32), (32, 0)]                            # C5
+    assert chunk_plan(7, 0, 2) == [(0, 2), (2, 2), (4, 0)]     # the odd item rides along
+    assert chunk_plan(5, 1, 2) == [(0, 2), (2, 0)]             # 2 pairs + a half item
+    assert chunk_plan(6, 2, 2) == [(0, 2), (2, 0)]             # 2 pairs + odd + half
+    assert chunk_plan(3, 1, 2) == [(0, 0)]
+    for n, part, c in [(40, 0, 8), (11, 0, 4), (9, 1, 2), (64, 0, 32)]:
+        plan = chunk_plan(n, part, c)
+        paired = (n - 1 if part else n) & ~1
+        covered = []
+        for f, cnt in plan:
+            assert f % 2 == 0 and (cnt == 0 or cnt % 2 == 0) and cnt <= c
+            end = f + cnt if cnt else n
+            covered += list(range(f, end))
+            assert min(end, paired) - f <= c
+        assert covered == list(range(n))
+    with pytest.raises(ValueError):
+        chunk_plan(9, 0, 3)
