@@ -195,6 +195,9 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
 #ifndef FWD_LPT_NOSPLIT
 #define FWD_LPT_NOSPLIT 0  // 1: longest-rays-first order for unsplit single-gate walks too
 #endif
+#ifndef FWD_LPT_SPLIT
+#define FWD_LPT_SPLIT 1    // longest-rays-first order for split single-gate walks
+#endif
 #ifndef FWD_MIN_BLOCKS_M
 #define FWD_MIN_BLOCKS_M 7        // single-item mirror walks (72 registers, no spills)
 #endif
@@ -1158,7 +1161,7 @@ cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st
         a.n_items = items;
         const int rest = items - np;
         const unsigned ngroup = mct_fwd_groups(mir_slots(a.A));
-        const bool lpt = (a.ksplit > 1 || FWD_LPT_NOSPLIT) && rest == 1;
+        const bool lpt = (a.ksplit > 1 ? FWD_LPT_SPLIT : FWD_LPT_NOSPLIT) && rest == 1;
         dim3 grid(lpt ? ngroup : ntile, lpt ? ntile : ngroup, rest * a.ksplit);
         if (lpt) {
             if (mode == 0)
