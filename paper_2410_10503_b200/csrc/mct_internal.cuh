@@ -173,7 +173,9 @@ __host__ __device__ __forceinline__ size_t mct_item_off(int item, int pair_items
 __host__ __device__ __forceinline__ size_t mct_img_off(int item, int pair_items, int asplit,
                                                        size_t slot_bytes, const WsGeom& g) {
     if (item >= pair_items) return (size_t)(item - pair_items) * g.item_bytes;
-    if (item < 2 * g.ring) return mct_pair_off(item >> 1, g) + g.pair_bytes + (item & 1) * g.pre_bytes;
+    if (item < 2 * g.ring)  // its pair's own block (pair < ring: no wrap)
+        return 2 * g.item_bytes + (size_t)(item >> 1) * g.pair_block + g.pair_bytes +
+               (item & 1) * g.pre_bytes;
     return 2 * g.item_bytes + (size_t)g.ring * g.pair_block +
            (size_t)(item - 2 * g.ring) * asplit * slot_bytes;
 }
@@ -227,6 +229,16 @@ struct ItemSel {
     int last_part;  // 0, or 1 / 2: the launch's last item covers the first / second half
     int first, count;  // K1-K3 chunk: items [first, first + count) (count 0: to the end)
 };
+
+// gate and absolute iteration of item k of slice `slice`
+__device__ __forceinline__ void resolve_slice_item(const ItemSel& s, int slice, int k, int& gate,
+                                                   int& iter) {
+    int e = s.epoch_ctr ? __ldg(s.epoch_ctr) : 0;
+    gate = s.gates ? __ldg(s.gates + (long long)slice * s.slice_stride +
+                           (long long)e * s.epoch_stride + s.base + k)
+                   : 0;
+    iter = s.epoch_ctr ? e * s.iters_per_epoch + s.iteration : s.iteration;
+}
 
 __device__ __forceinline__ void resolve_item(const ItemSel& s, int item, int& slice, int& gate,
                                              int& iter) {

@@ -55,8 +55,8 @@ update_kernel(UpdArgs p) {
     const int np = mct_pair_items(p.sel.ips * p.sel.num_slices, p.sel.last_part);
     for (int k = lane; k < p.sel.ips; k += LANES) {
         const int item = slice * p.sel.ips + k;
-        int s_, gate, iter;
-        resolve_item(p.sel, item, s_, gate, iter);
+        int gate, iter;
+        resolve_slice_item(p.sel, slice, k, gate, iter);
         const char* img = p.img_override
                               ? reinterpret_cast<const char*>(p.img_override)
                               : p.ws + mct_img_off(item, np, p.asplit, p.img_slot_bytes, p.wsg) +
@@ -83,7 +83,7 @@ update_kernel(UpdArgs p) {
         if (p.warps == nullptr) {
             v = fetch(q);
         } else {
-            const WarpDesc& wd = p.warps[p.sel.gates ? (long long)slice * p.N + gate : 0];
+            const WarpT wd = load_warp_t(p.warps + (p.sel.gates ? (long long)slice * p.N + gate : 0));
             v = warp_adjoint_at(wd, fetch, qr, qc);
         }
         sum += v;

@@ -91,8 +91,29 @@ __device__ __forceinline__ float warp_apply_at(const WarpDesc& w, int r, int c, 
 // of w(p, q) * y[p], reading y through `fetch(flat_index)`.  The plan's
 // transposed gather list (sorted by p, built from warp_taps itself) makes the
 // weights bit-identical to the forward's and the order fixed (deterministic).
+// The adjoint's view of a warp descriptor, held in registers (a WarpDesc in global
+// memory would be re-read for every entry: the compiler cannot prove it unaliased).
+struct WarpT {
+    int kind, cols;
+    const int* tptr;
+    const int* tidx;
+    const float* tw;
+};
+__device__ __forceinline__ WarpT load_warp_t(const WarpDesc* d) {
+    WarpT w;
+    w.kind = __ldg(&d->kind);
+    w.cols = __ldg(&d->cols);
+    w.tptr = reinterpret_cast<const int*>(
+        __ldg(reinterpret_cast<const unsigned long long*>(&d->tptr)));
+    w.tidx = reinterpret_cast<const int*>(
+        __ldg(reinterpret_cast<const unsigned long long*>(&d->tidx)));
+    w.tw = reinterpret_cast<const float*>(
+        __ldg(reinterpret_cast<const unsigned long long*>(&d->tw)));
+    return w;
+}
+
 template <typename Fetch>
-__device__ __forceinline__ float warp_adjoint_at(const WarpDesc& w, Fetch fetch, int qr, int qc) {
+__device__ __forceinline__ float warp_adjoint_at(const WarpT& w, Fetch fetch, int qr, int qc) {
     const long long q = (long long)qr * w.cols + qc;
     if (w.kind == MCT_WARP_IDENTITY) return fetch(q);
     const int e0 = __ldg(w.tptr + q), e1 = __ldg(w.tptr + q + 1);
