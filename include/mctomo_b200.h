@@ -49,7 +49,8 @@ const char* mct_last_error(void);
  * cos_a, sin_a, rows_dominant are HOST arrays of length num_angles computed by
  * the caller exactly as projector._build_tables does (projector.py:127-130:
  * angles = arange(A)*(pi/A); cos, sin; |cos| >= sin).  Detector bin centres
- * follow Geometry.bin_centers (projector.py:75-79).                            */
+ * follow Geometry.bin_centers (projector.py:75-79).  Images hold at most 2^29
+ * pixels (32-bit element offsets, int32 warp-list entries): MCT_ERR_ARG beyond.  */
 typedef struct mct_ray_plan mct_ray_plan;
 
 int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,

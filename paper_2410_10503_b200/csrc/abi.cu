@@ -205,6 +205,7 @@ int mct_ray_plan_create(mct_ray_plan** plan, int rows, int cols, int num_angles,
     // Geometry.__post_init__ (projector.py:63-68)
     MCT_REQUIRE(rows >= 1, "rows must be >= 1");
     MCT_REQUIRE(cols >= 1, "cols must be >= 1");
+    MCT_REQUIRE((long long)rows * cols <= MCT_MAX_PIXELS, "images above 2^29 pixels are not supported");
     MCT_REQUIRE(num_angles >= 1, "num_angles must be >= 1");
     MCT_REQUIRE(num_bins >= 1, "num_bins must be >= 1");
     MCT_REQUIRE(spacing > 0 && isfinite(spacing), "detector_spacing must be positive");
@@ -425,7 +426,8 @@ static int warp_finish(mct_warp_plan* p, mct_warp_plan** out) {
 int mct_warp_plan_create_identity(mct_warp_plan** plan, int rows, int cols) {
     MCT_REQUIRE(plan, "plan out-pointer is null");
     *plan = nullptr;
-    MCT_REQUIRE(rows >= 1 && cols >= 1, "invalid image shape");
+    MCT_REQUIRE(rows >= 1 && cols >= 1 && (long long)rows * cols <= MCT_MAX_PIXELS,
+                "invalid image shape");
     mct_warp_plan* p = new mct_warp_plan();
     p->desc = identity_desc(rows, cols);
     return warp_finish(p, plan);
@@ -435,7 +437,8 @@ int mct_warp_plan_create_rigid(mct_warp_plan** plan, int rows, int cols, double 
                                double sin_r, double t_row, double t_col) {
     MCT_REQUIRE(plan, "plan out-pointer is null");
     *plan = nullptr;
-    MCT_REQUIRE(rows >= 1 && cols >= 1, "invalid image shape");
+    MCT_REQUIRE(rows >= 1 && cols >= 1 && (long long)rows * cols <= MCT_MAX_PIXELS,
+                "invalid image shape");
     MCT_REQUIRE(isfinite(cos_r) && isfinite(sin_r) && isfinite(t_row) && isfinite(t_col),
                 "motion parameters must be finite");
     mct_warp_plan* p = new mct_warp_plan();
@@ -457,7 +460,8 @@ int mct_warp_plan_create_rigid(mct_warp_plan** plan, int rows, int cols, double 
 int mct_warp_plan_create_dilatation(mct_warp_plan** plan, int rows, int cols, double scale) {
     MCT_REQUIRE(plan, "plan out-pointer is null");
     *plan = nullptr;
-    MCT_REQUIRE(rows >= 1 && cols >= 1, "invalid image shape");
+    MCT_REQUIRE(rows >= 1 && cols >= 1 && (long long)rows * cols <= MCT_MAX_PIXELS,
+                "invalid image shape");
     MCT_REQUIRE(scale > 0 && isfinite(scale), "scale must be positive");
     mct_warp_plan* p = new mct_warp_plan();
     WarpDesc d = identity_desc(rows, cols);
@@ -476,7 +480,8 @@ int mct_warp_plan_create_dense(mct_warp_plan** plan, int rows, int cols, const f
                                void* stream) {
     MCT_REQUIRE(plan, "plan out-pointer is null");
     *plan = nullptr;
-    MCT_REQUIRE(rows >= 1 && cols >= 1, "invalid image shape");
+    MCT_REQUIRE(rows >= 1 && cols >= 1 && (long long)rows * cols <= MCT_MAX_PIXELS,
+                "invalid image shape");
     MCT_REQUIRE(phi_dev, "phi is null");
     cudaStream_t st = (cudaStream_t)stream;
     const long long n = (long long)rows * cols;

@@ -28,6 +28,9 @@
 #include "../../include/mctomo_b200.h"
 
 #define MCT_PADX 4
+// image size limit: 32-bit tap indices in K2 / K3 and int32 entries in the transposed
+// warp lists (about 4 per pixel)
+#define MCT_MAX_PIXELS (1LL << 29)
 
 // ---------------------------------------------------------------- ray plan --
 // Forward (ray-driven) per-angle constants.  projector.py:134-155 restated as

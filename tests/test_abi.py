@@ -51,6 +51,7 @@ def test_sm100a_cubin_embedded():
     ((0, 8, 4, 8, 1.0), "rows"),
     ((8, 8, 0, 8, 1.0), "num_angles"),
     ((8, 8, 4, 8, -1.0), "detector_spacing"),
+    ((32768, 32768, 4, 8, 1.0), "2\\^29 pixels"),
 ])
 def test_plan_validation_maps_to_value_error(args, msg):
     L = _lib.load()
