@@ -401,10 +401,11 @@ int mct_ray_adjoint(const mct_ray_plan* rp, const float* sino, float* img, int b
 // on the device from the forward's own taps, so forward and adjoint weights are
 // bit-identical.  Synchronous (plan construction only).
 static cudaError_t attach_transpose(mct_warp_plan* p, cudaStream_t st) {
-    cudaError_t e = build_dense_transpose(p->desc, &p->tptr, &p->tent, &p->nnz, st);
+    cudaError_t e = build_dense_transpose(p->desc, &p->tptr, &p->tidx, &p->tw, &p->nnz, st);
     if (e != cudaSuccess) return e;
     p->desc.tptr = p->tptr;
-    p->desc.tent = p->tent;
+    p->desc.tidx = p->tidx;
+    p->desc.tw = p->tw;
     return cudaSuccess;
 }
 
@@ -415,7 +416,8 @@ static int warp_finish(mct_warp_plan* p, mct_warp_plan** out) {
         cudaFree(p->d_desc);
         cudaFree(p->phi);
         cudaFree(p->tptr);
-        cudaFree(p->tent);
+        cudaFree(p->tidx);
+        cudaFree(p->tw);
         delete p;
         return cuda_fail(e, "warp plan");
     }
@@ -510,14 +512,15 @@ int mct_warp_plan_create_dense(mct_warp_plan** plan, int rows, int cols, const f
         return mct_set_error(MCT_ERR_ARG, "displacement field magnitude exceeds 1e6 pixels");
     }
     d.phi = p->phi;
-    if (e == cudaSuccess) e = build_dense_transpose(d, &p->tptr, &p->tent, &p->nnz, st);
+    if (e == cudaSuccess) e = build_dense_transpose(d, &p->tptr, &p->tidx, &p->tw, &p->nnz, st);
     if (e != cudaSuccess) {
         cudaFree(p->phi);
         delete p;
         return cuda_fail(e, "mct_warp_plan_create_dense");
     }
     d.tptr = p->tptr;
-    d.tent = p->tent;
+    d.tidx = p->tidx;
+    d.tw = p->tw;
     p->desc = d;
     return warp_finish(p, plan);
 }
@@ -527,7 +530,8 @@ int mct_warp_plan_destroy(mct_warp_plan* plan) {
     cudaFree(plan->d_desc);
     cudaFree(plan->phi);
     cudaFree(plan->tptr);
-    cudaFree(plan->tent);
+    cudaFree(plan->tidx);
+    cudaFree(plan->tw);
     delete plan;
     return MCT_OK;
 }

@@ -197,7 +197,8 @@ struct WarpDesc {
     double scale;            // dilatation
     const float* phi;        // dense (2, rows, cols)
     const int* tptr;         // transposed gather list of D (rows*cols + 1), all non-identity kinds
-    const int2* tent;        // its entries: (source pixel, weight bits), one 8-byte load each
+    const int* tidx;
+    const float* tw;
 };
 
 struct mct_warp_plan {
@@ -205,7 +206,8 @@ struct mct_warp_plan {
     WarpDesc* d_desc;  // device copy of desc
     float* phi;
     int* tptr;
-    int2* tent;
+    int* tidx;
+    float* tw;
     long long nnz;
 };
 
@@ -358,8 +360,8 @@ cudaError_t launch_axpby_mixed(long long n, double alpha, const void* x, int xf6
 cudaError_t launch_dot_f64(const double* a, const double* b, long long n, double* out,
                            double* scratch, cudaStream_t st);
 cudaError_t launch_absmax(const float* x, long long n, float* out, cudaStream_t st);
-cudaError_t build_dense_transpose(const WarpDesc& desc, int** tptr, int2** tent, long long* nnz,
-                                  cudaStream_t st);
+cudaError_t build_dense_transpose(const WarpDesc& desc, int** tptr, int** tidx, float** tw,
+                                  long long* nnz, cudaStream_t st);
 
 cudaError_t launch_gaussian_field(unsigned long long k0, unsigned long long k1, long long count,
                                   double scale, const float* base, void* out, int out_f64,

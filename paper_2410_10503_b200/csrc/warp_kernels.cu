@@ -157,7 +157,7 @@ __global__ void dense_count_kernel(WarpDesc wd, int* cnt) {
         }
 }
 
-__global__ void dense_fill_kernel(WarpDesc wd, int* cursor, int2* tent) {
+__global__ void dense_fill_kernel(WarpDesc wd, int* cursor, int* tidx, float* tw) {
     const long long n = (long long)wd.rows * wd.cols;
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
@@ -169,25 +169,29 @@ __global__ void dense_fill_kernel(WarpDesc wd, int* cursor, int2* tent) {
             float w = tap_weight(t, dr, dc);
             if (rr >= 0 && rr < wd.rows && cc >= 0 && cc < wd.cols && w != 0.0f) {
                 int pos = atomicAdd(cursor + (long long)rr * wd.cols + cc, 1);
-                tent[pos] = make_int2((int)p, __float_as_int(w));
+                tidx[pos] = (int)p;
+                tw[pos] = w;
             }
         }
 }
 
 // Sort each (short) segment by source pixel so the gather order — and hence the
 // fp32 sum — is independent of atomic arrival order.
-__global__ void dense_sort_kernel(long long n, const int* tptr, int2* tent) {
+__global__ void dense_sort_kernel(long long n, const int* tptr, int* tidx, float* tw) {
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n) return;
     const int e0 = tptr[q], e1 = tptr[q + 1];
     for (int i = e0 + 1; i < e1; ++i) {
-        const int2 key = tent[i];
+        int key = tidx[i];
+        float w = tw[i];
         int k = i - 1;
-        while (k >= e0 && tent[k].x > key.x) {
-            tent[k + 1] = tent[k];
+        while (k >= e0 && tidx[k] > key) {
+            tidx[k + 1] = tidx[k];
+            tw[k + 1] = tw[k];
             --k;
         }
-        tent[k + 1] = key;
+        tidx[k + 1] = key;
+        tw[k + 1] = w;
     }
 }
 
@@ -392,11 +396,11 @@ cudaError_t launch_absmax(const float* x, long long n, float* out, cudaStream_t 
 }
 
 // Synchronous (plan construction only).
-cudaError_t build_dense_transpose(const WarpDesc& desc, int** tptr_out, int2** tent_out,
-                                  long long* nnz_out, cudaStream_t st) {
+cudaError_t build_dense_transpose(const WarpDesc& desc, int** tptr_out, int** tidx_out,
+                                  float** tw_out, long long* nnz_out, cudaStream_t st) {
     const long long n = (long long)desc.rows * desc.cols;
-    int *cnt = nullptr, *tptr = nullptr;
-    int2* tent = nullptr;
+    int *cnt = nullptr, *tptr = nullptr, *tidx = nullptr;
+    float* tw = nullptr;
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
     int total = 0;
@@ -417,24 +421,27 @@ cudaError_t build_dense_transpose(const WarpDesc& desc, int** tptr_out, int2** t
     CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, tptr, (int)(n + 1), st));
     CK(cudaMemcpyAsync(&total, tptr + n, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    CK(cudaMalloc(&tent, (size_t)(total > 0 ? total : 1) * sizeof(int2)));
+    CK(cudaMalloc(&tidx, (size_t)(total > 0 ? total : 1) * sizeof(int)));
+    CK(cudaMalloc(&tw, (size_t)(total > 0 ? total : 1) * sizeof(float)));
     CK(cudaMemcpyAsync(cnt, tptr, n * sizeof(int), cudaMemcpyDeviceToDevice, st));
-    dense_fill_kernel<<<nb, 256, 0, st>>>(desc, cnt, tent);
+    dense_fill_kernel<<<nb, 256, 0, st>>>(desc, cnt, tidx, tw);
     CK(cudaGetLastError());
-    dense_sort_kernel<<<nb, 256, 0, st>>>(n, tptr, tent);
+    dense_sort_kernel<<<nb, 256, 0, st>>>(n, tptr, tidx, tw);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     cudaFree(cnt);
     cudaFree(tmp);
     *tptr_out = tptr;
-    *tent_out = tent;
+    *tidx_out = tidx;
+    *tw_out = tw;
     *nnz_out = total;
     return cudaSuccess;
 fail:
     cudaFree(cnt);
     cudaFree(tmp);
     cudaFree(tptr);
-    cudaFree(tent);
+    cudaFree(tidx);
+    cudaFree(tw);
     return e;
 #undef CK
 }

@@ -96,7 +96,8 @@ __device__ __forceinline__ float warp_apply_at(const WarpDesc& w, int r, int c, 
 struct WarpT {
     int kind, cols;
     const int* tptr;
-    const int2* tent;
+    const int* tidx;
+    const float* tw;
 };
 __device__ __forceinline__ WarpT load_warp_t(const WarpDesc* d) {
     WarpT w;
@@ -104,8 +105,10 @@ __device__ __forceinline__ WarpT load_warp_t(const WarpDesc* d) {
     w.cols = __ldg(&d->cols);
     w.tptr = reinterpret_cast<const int*>(
         __ldg(reinterpret_cast<const unsigned long long*>(&d->tptr)));
-    w.tent = reinterpret_cast<const int2*>(
-        __ldg(reinterpret_cast<const unsigned long long*>(&d->tent)));
+    w.tidx = reinterpret_cast<const int*>(
+        __ldg(reinterpret_cast<const unsigned long long*>(&d->tidx)));
+    w.tw = reinterpret_cast<const float*>(
+        __ldg(reinterpret_cast<const unsigned long long*>(&d->tw)));
     return w;
 }
 
@@ -123,9 +126,8 @@ __device__ __forceinline__ float warp_adjoint_at(const WarpT& w, Fetch fetch, in
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const bool ok = e + j < e1;
-            const int2 ent = ok ? __ldg(w.tent + e + j) : make_int2(-1, 0);
-            idx[j] = ent.x;
-            wt[j] = __int_as_float(ent.y);
+            idx[j] = ok ? __ldg(w.tidx + e + j) : -1;
+            wt[j] = ok ? __ldg(w.tw + e + j) : 0.0f;
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) v[j] = idx[j] >= 0 ? fetch(idx[j]) : 0.0f;
