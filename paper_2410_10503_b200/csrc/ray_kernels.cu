@@ -546,8 +546,12 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
 #endif
 #define ADJ_STAGED(K, G) ((K) == 0 && ((G) == 2 ? ADJ_TMA : ADJ_TMA1))
 #ifndef ADJ_TC
-#define ADJ_TC 4       // angle pairs per TMA stage
+#define ADJ_TC 4       // angle pairs per TMA stage (gate pairs)
 #endif
+#ifndef ADJ_TC1
+#define ADJ_TC1 6      // angle pairs per TMA stage (single items: half the bytes per pair)
+#endif
+#define ADJ_TCG(G) ((G) == 2 ? ADJ_TC : ADJ_TC1)
 #ifndef ADJ_NST
 #define ADJ_NST 2      // stage buffers (ring): one computed, NST - 1 in flight
 #endif
@@ -721,7 +725,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
     __shared__ double s_tot[G][2 * PPT][ADJ_THREADS];
     // TMA staging (K = 0): per angle pair the block's sinogram segments -- the bins
     // under the tile's primary columns and under its mirror columns, in row a (and
-    // row A-a, G = 2) -- first element and length; two stage buffers of ADJ_TC pairs
+    // row A-a, G = 2) -- first element and length; two stage buffers of ADJ_TCG(G) pairs
     __shared__ int4 s_lo[ADJ_STAGED(K, G) ? ADJ_CH : 1];
     __shared__ unsigned long long s_full[ADJ_NST];
     extern __shared__ float4 s_stage[];
@@ -853,12 +857,12 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
             // async-proxy fence before the TMA writes)
             constexpr int NSEG = G == 2 ? 4 : 2;
             constexpr int segw = ADJ_SEGW;
-            const int nst = (cnt + ADJ_TC - 1) / ADJ_TC;
+            const int nst = (cnt + ADJ_TCG(G) - 1) / ADJ_TCG(G);
             auto issue = [&](int st) {  // stage st of this chunk (ring use uses + st)
                 const unsigned u = uses + (unsigned)st;
                 const int b = (int)(u % ADJ_NST);
                 fence_proxy_async();
-                const int t0 = st * ADJ_TC, t1 = min(cnt, t0 + ADJ_TC);
+                const int t0 = st * ADJ_TCG(G), t1 = min(cnt, t0 + ADJ_TCG(G));
                 unsigned bytes = 0;
                 for (int t = t0; t < t1; ++t) {
                     const int4 L = s_lo[t];
@@ -867,7 +871,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
                 mbar_expect_tx(&s_full[b], bytes);
                 for (int t = t0; t < t1; ++t) {
                     const int4 L = s_lo[t];
-                    float4* dst = s_stage + (size_t)(b * ADJ_TC + (t - t0)) * NSEG * segw;
+                    float4* dst = s_stage + (size_t)(b * ADJ_TCG(G) + (t - t0)) * NSEG * segw;
                     tma_load_1d(dst, DY2 + L.x, L.y * 16u, &s_full[b]);
                     tma_load_1d(dst + segw, DY2 + L.z, L.w * 16u, &s_full[b]);
                     if (G == 2) {
@@ -888,7 +892,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
                 const unsigned u = uses + (unsigned)st;
                 const int b = (int)(u % ADJ_NST);
                 mbar_wait(&s_full[b], (u / ADJ_NST) & 1u);
-                const int t0 = st * ADJ_TC, t1 = min(cnt, t0 + ADJ_TC);
+                const int t0 = st * ADJ_TCG(G), t1 = min(cnt, t0 + ADJ_TCG(G));
                 // FULL: all PPT rows in the image (warp-uniform), no per-row guard
                 auto stage = [&](auto full) {
                     constexpr bool FULL = decltype(full)::value;
@@ -906,7 +910,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
                         unsigned mlo = (unsigned)Tm, mhi = (unsigned)(Tm >> 32);
                         // segments: [primary, row a | mirror, row a | primary, row A-a |
                         // mirror, row A-a], each segw elements
-                        const float4* sb = s_stage + (size_t)(b * ADJ_TC + (t - t0)) * NSEG * segw;
+                        const float4* sb = s_stage + (size_t)(b * ADJ_TCG(G) + (t - t0)) * NSEG * segw;
 #pragma unroll
                         for (int m = 0; m < PPT; ++m) {
                             if (FULL || m < nrows) {
@@ -1231,7 +1235,7 @@ int adj_segw(const mct_ray_plan* rp) {
 // not fit ADJ_SEGW (launch_adj_g then runs the unstaged runtime-footprint kernel).
 size_t adj_stage_bytes(int G, int segw) {
     return ADJ_STAGED(0, G) && segw <= ADJ_SEGW
-               ? (size_t)ADJ_NST * ADJ_TC * (G == 2 ? 4 : 2) * ADJ_SEGW * sizeof(float4)
+               ? (size_t)ADJ_NST * ADJ_TCG(G) * (G == 2 ? 4 : 2) * ADJ_SEGW * sizeof(float4)
                : 0;
 }
 
