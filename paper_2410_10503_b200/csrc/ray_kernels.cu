@@ -552,6 +552,12 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
 #define ADJ_TC1 6      // angle pairs per TMA stage (single items: half the bytes per pair)
 #endif
 #define ADJ_TCG(G) ((G) == 2 ? ADJ_TC : ADJ_TC1)
+#ifndef ADJ_STU2
+#define ADJ_STU2 4     // unroll of the staged angle-pair loop (gate pairs: a whole stage)
+#endif
+#ifndef ADJ_STU1
+#define ADJ_STU1 6     // ... (single items: a whole stage)
+#endif
 #ifndef ADJ_NST
 #define ADJ_NST 2      // stage buffers (ring): one computed, NST - 1 in flight
 #endif
@@ -896,7 +902,8 @@ __global__ void __launch_bounds__(ADJ_THREADS, AdjShape<G>::MINB) adj_kernel(Adj
                 // FULL: all PPT rows in the image (warp-uniform), no per-row guard
                 auto stage = [&](auto full) {
                     constexpr bool FULL = decltype(full)::value;
-#pragma unroll 2
+                    constexpr int SU = G == 2 ? ADJ_STU2 : ADJ_STU1;
+#pragma unroll (SU)
                     for (int t = t0; t < t1; ++t) {
                         const longlong2 T2 = s_t[t];
                         const int4 U = s_u[t];
