@@ -217,3 +217,28 @@ def test_chunked_gate_shard_rank_with_half_item(m, half):
     assert len(eng.chunks(eng.local, 0 if half is None else half[1])) == 2
     for (dz0, y0, x0), (dz1, y1, x1) in zip(ref, out):
         assert np.array_equal(dz0, dz1) and np.array_equal(y0, y1) and np.array_equal(x0, x1)
+
+
+def test_ring_setter_validation_and_kernel_timer(m):
+    """mct_ray_plan_set_ring_pairs rejects < 1 (ValueError through the binding); the
+    KernelTimer marks of a chunked iteration give one K1-K3 mark per chunk, one K4 mark,
+    and positive per-kernel times."""
+    import torch
+
+    from paper_2410_10503_b200 import projector, workloads
+    from paper_2410_10503_b200.engine import Engine, KernelTimer
+
+    projector.ray_transform.cache_clear()
+    cfgw = workloads.WorkloadConfig("ring_t", 32, 30, 47, 6, "rigid", 3, 1e-2, 1)
+    prob, _ = fresh_problem(m, cfgw, 0, 1)
+    plan = prob.operators[0].outer.plan()
+    with pytest.raises(ValueError):
+        plan.set_ring_pairs(0)
+    eng = Engine([prob.operators], [prob.data])
+    eng.set_params(m.default_config("pdhg", [30.0] * 6, cfgw.alpha, 1, stacked_norm_sq=5400.0))
+    timer = KernelTimer(torch)
+    eng.iteration(eng.items_pdhg(), cfgw.alpha, mark=timer)
+    torch.cuda.synchronize()
+    assert timer.launches() == [3, 3, 3, 1]
+    assert all(t > 0 for t in timer.times_ms())
+    projector.ray_transform.cache_clear()
