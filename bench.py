@@ -129,6 +129,39 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+# ------------------------------------------------------------ e2e read-back
+class ReadBack:
+    """Device -> host read of every step's result x without stalling the next step:
+    x is snapshotted on the compute stream (device copy, a few µs) and the D2H of the
+    snapshot runs on its own stream into pinned memory, double-buffered; a snapshot
+    buffer is rewritten only after its previous D2H finished."""
+
+    def __init__(self, torch, x, stream):
+        self.torch, self.stream = torch, stream
+        self.stage = [torch.empty_like(x) for _ in range(2)]
+        self.host = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for _ in range(2)]
+        self.snap = [torch.cuda.Event(), torch.cuda.Event()]
+        self.back = [torch.cuda.Event(), torch.cuda.Event()]
+        self.s = torch.cuda.Stream()
+        self.k = 0
+        self.bytes = int(x.numel() * x.element_size())
+
+    def read(self, x):
+        b = self.k & 1
+        if self.k >= 2:
+            self.stream.wait_event(self.back[b])
+        self.stage[b].copy_(x, non_blocking=True)
+        self.snap[b].record(self.stream)
+        with self.torch.cuda.stream(self.s):
+            self.s.wait_event(self.snap[b])
+            self.host[b].copy_(self.stage[b], non_blocking=True)
+            self.back[b].record(self.s)
+        self.k += 1
+
+    def finish(self):
+        self.stream.wait_stream(self.s)
+
+
 # ------------------------------------------------------- algorithmic bytes
 def alg_bytes(cfg):
     """SURVEY.md §8d SpMV-equivalent fp32 bytes (4 B per nonzero operand / output)."""
@@ -560,7 +593,7 @@ def run_ours(args, cfg):
         glo, ghi = (worker.data_lo, worker.data_hi) if use_dist else (0, cfg.num_gates)
         host_d = torch.from_numpy(np.stack([np.asarray(d, dtype=np.float32)
                                             for d in problem.data[glo:ghi]])[None]).pin_memory()
-        host_x = torch.empty(eng.x.shape, dtype=torch.float32).pin_memory()
+        back = ReadBack(torch, eng.x, stream)
         d_bufs = [eng.d, torch.empty_like(eng.d)]
         runners = []
         for b in range(2):
@@ -587,7 +620,7 @@ def run_ours(args, cfg):
                     eng.set_data_buffer(d_bufs[b])
                 runners[b]()
                 ev_done[b].record(stream)
-                host_x.copy_(eng.x, non_blocking=True)   # the step's result, D2H
+                back.read(eng.x)                          # the step's result, D2H
                 if k + 1 < K:
                     nb = 1 - b
                     with torch.cuda.stream(copy_s):
@@ -596,6 +629,7 @@ def run_ours(args, cfg):
                         d_bufs[nb][:, glo:ghi].copy_(host_d, non_blocking=True)
                         ev_copied[nb].record(copy_s)
             stream.wait_stream(copy_s)
+            back.finish()
 
         e2e_run(2)
         barrier()
@@ -604,8 +638,12 @@ def run_ours(args, cfg):
         e2e = {"value": 1000.0 / e_ms, "unit": "epochs/s",
                # whole job: every gate's sinogram once, x read back on every rank
                "h2d_bytes_per_step": int(cfg.num_gates * cfg.num_angles * cfg.num_bins * 4),
-               "d2h_bytes_per_step": int(host_x.numel() * 4) * world,
-               "overlap": "H2D of step k+1 (copy stream, double-buffered) overlaps step k"}
+               "d2h_bytes_per_step": back.bytes * world,
+               "overlap": "H2D of step k+1 (copy stream, double-buffered) overlaps step k; the "
+                          "D2H of x reads a device snapshot on a third stream",
+               "launch": ("one CUDA graph per epoch, as run() launches it (`value` times eager "
+                          "launches with a CUDA event between the kernels, about 1 % slower)"
+                          if not use_dist else "eager launches (gate-sharded step)")}
 
     # ---------------- CPU baseline (rank 0, N=1) ----------------------------
     cpu = None
@@ -750,7 +788,7 @@ def run_batch_ours(args, cfg):
     e2e = None
     if not args.no_e2e:
         host_d = eng.d.cpu().pin_memory()
-        host_x = torch.empty(eng.x.shape, dtype=torch.float32).pin_memory()
+        back = ReadBack(torch, eng.x, stream)
         d_bufs = [eng.d, torch.empty_like(eng.d)]
         graphs = []
         for b in range(2):
@@ -770,7 +808,7 @@ def run_batch_ours(args, cfg):
                 stream.wait_event(ev_copied[b])
                 graphs[b].replay()
                 ev_done[b].record(stream)
-                host_x.copy_(eng.x, non_blocking=True)
+                back.read(eng.x)
                 if k + 1 < K:
                     nb = 1 - b
                     with torch.cuda.stream(copy_s):
@@ -779,6 +817,7 @@ def run_batch_ours(args, cfg):
                         d_bufs[nb].copy_(host_d, non_blocking=True)
                         ev_copied[nb].record(copy_s)
             stream.wait_stream(copy_s)
+            back.finish()
 
         eng.reset()  # epoch counter back to 0: the drawn gate sequences cover warmup + steps
         e2e_run(1)
@@ -788,8 +827,9 @@ def run_batch_ours(args, cfg):
         eng.set_data_buffer(d_bufs[0])
         e2e = {"value": 1000.0 / e_ms, "unit": "epochs/s",
                "h2d_bytes_per_step": int(host_d.numel() * 4) * world,
-               "d2h_bytes_per_step": int(host_x.numel() * 4) * world,
-               "overlap": "H2D of step k+1 (copy stream, double-buffered) overlaps step k"}
+               "d2h_bytes_per_step": back.bytes * world,
+               "overlap": "H2D of step k+1 (copy stream, double-buffered) overlaps step k; the "
+                          "D2H of x reads a device snapshot on a third stream"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
