@@ -18,7 +18,10 @@ device synchronize, CUDA events on the launching stream, max over ranks.  The
 per-epoch working set (data + duals + workspace ~ 0.8 GB) exceeds the 126 MB L2,
 so no explicit flush is needed (stated in ``config``).  ``e2e`` repeats the
 measurement through the C-ABI with the step's inputs (the 20 gated sinograms)
-copied host->device from pinned memory and the result x copied back every step.
+copied host->device from pinned memory and the result x copied back every step
+(uploads double-buffered on a copy stream, the read-back from a device snapshot on a
+third stream, the epoch launched as the CUDA graph ``run()`` uses; ``value`` times eager
+launches with a CUDA event between the kernels, which is about 1 % slower).
 
 ``--impl reference`` times the CPU restatement of the reference (oracle/, fp64 C,
 all host threads) on a bounded sample of the same workload.
