@@ -190,7 +190,7 @@ __device__ __forceinline__ void fx_sub(unsigned& lo, unsigned& hi, unsigned ilo,
 #endif
 #define FWD_ANGLES MCT_FWD_ANGLES  // warps (= consecutive angles) per block; they share L1 lines
 #ifndef FWD_MIN_BLOCKS2
-#define FWD_MIN_BLOCKS2 8         // gate pairs: 8 x 4 warps resident, 64 registers
+#define FWD_MIN_BLOCKS2 16        // gate pairs: 16 x 2 warps resident, 64 registers
 #endif
 #ifndef FWD_LPT_NOSPLIT
 #define FWD_LPT_NOSPLIT 0  // 1: longest-rays-first order for unsplit single-gate walks too
@@ -220,7 +220,8 @@ __device__ __forceinline__ float dhi(const float4& v, int h) { return h ? v.w : 
 // Every per-ray sum is accumulated as by the one-ray walk: 8 samples per trip,
 // fp32 partial sums per 64 samples, fp64 totals.
 template <int MODE, int LPT, int MIR>
-__global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_MIN_BLOCKS2)
+__global__ void __launch_bounds__(32 * (MIR ? FWD_ANGLES : MCT_FWD_ANGLES_P),
+                                  MIR ? FWD_MIN_BLOCKS_M : FWD_MIN_BLOCKS2)
     fwd_kernel(FwdArgs p) {
     using V = float4;
     constexpr int G = 2;
@@ -245,7 +246,8 @@ __global__ void __launch_bounds__(32 * FWD_ANGLES, MIR ? FWD_MIN_BLOCKS_M : FWD_
     // delivers a 16-byte request in 4 clocks while 8 consecutive lanes stay inside 128
     // bytes, 8 clocks once they spread further (tools/micro/l1_pattern.cu)
     constexpr int IL = MCT_FWD_IL, BW = 32 / IL;
-    const int s_raw = ((LPT ? blockIdx.x : blockIdx.y) * FWD_ANGLES + threadIdx.y) * IL +
+    constexpr int NW = MIR ? FWD_ANGLES : MCT_FWD_ANGLES_P;  // warps per block
+    const int s_raw = ((LPT ? blockIdx.x : blockIdx.y) * NW + threadIdx.y) * IL +
                       (int)threadIdx.x % IL;
     const int nslot = MIR ? mir_slots(p.A) : p.A;
     bool warp_on = s_raw < nslot;            // per lane; no early exit (block syncs below)
@@ -1143,7 +1145,7 @@ static cudaError_t fork_join(cudaStream_t st, MainF main_launch, SideF side_laun
 
 cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st) {
     fwd_prefer_l1();
-    const dim3 block(32, FWD_ANGLES);
+    const dim3 block(32, FWD_ANGLES), block_p(32, MCT_FWD_ANGLES_P);
     const unsigned ntile = mct_fwd_btiles(a_in.B);
     const int np = mct_pair_items(items, a_in.sel.last_part);
     // this chunk's paired items [p_lo, p_hi); the unpaired tail runs with the last chunk
@@ -1156,11 +1158,11 @@ cudaError_t launch_fwd(const FwdArgs& a_in, int mode, int items, cudaStream_t st
         a.item0 = p_lo;
         a.n_items = items;
         a.ksplit = 1;  // >= 2 items fill the GPU without splitting rays (no partials)
-        dim3 grid(ntile, mct_fwd_groups(a.A), ((p_hi - p_lo) / 2) * a.ksplit);
+        dim3 grid(ntile, mct_fwd_groups(a.A, MCT_FWD_ANGLES_P), ((p_hi - p_lo) / 2) * a.ksplit);
         if (mode == 0)
-            fwd_kernel<0, 0, 0><<<grid, block, 0, s>>>(a);
+            fwd_kernel<0, 0, 0><<<grid, block_p, 0, s>>>(a);
         else
-            fwd_kernel<1, 0, 0><<<grid, block, 0, s>>>(a);
+            fwd_kernel<1, 0, 0><<<grid, block_p, 0, s>>>(a);
     };
     // single items (mirror-angle walks; an odd last item after the pairs).  One
     // single-gate item: longest-rays-first dispatch order (LPT) shrinks the last
